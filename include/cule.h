@@ -1,0 +1,137 @@
+/*
+ * cule.h — C-ABI of libcule: batched Atari 2600 emulation on one B200 (sm_100a).
+ *
+ * The hot path of CuLE (Dalton, Frosio & Garland, arXiv 1907.08467): thousands of independent
+ * consoles each step a 6502 CPU + RIOT + TIA for `frameskip` frames per action, render the
+ * frames the observation needs, reduce them to an observation, decode reward and terminal from
+ * RAM, and reset finished environments from a cache of random initial states.
+ *
+ *   PAPER.md P:252-276  one console = 6502 + TIA + 128 B RAM + ROM, 160x210 frames in GPU memory
+ *   PAPER.md P:280-284  only the last two frames of an action window are rendered; pixel-wise max
+ *   PAPER.md P:290-300  reset from a cache of random initial states (64 startup + up to 30 random)
+ *   PAPER.md P:540-541  84x84 grayscale observations
+ *   SPEC.md  S:530-573  flat create/step/reset/close API, buffer reuse, error classes
+ * Hardware details the paper does not give follow the written model in DESIGN.md §2 (the same
+ * model the CPU oracle implements independently).
+ *
+ * Conventions for every call:
+ *   - returns 0 (CULE_OK) or a negative CULE_E_* code; cule_last_error() gives a message
+ *     (thread-local, valid until the next call on the same thread);
+ *   - "d_" pointers are DEVICE pointers on the handle's device, "h_" pointers are HOST pointers;
+ *   - the caller owns all device memory (workspace, actions, observations, rewards, dones,
+ *     counters) and keeps it alive while the handle uses it; the library never allocates device
+ *     memory;
+ *   - calls taking `cuda_stream` (a cudaStream_t, NULL = legacy default stream) are asynchronous
+ *     on that stream unless stated; a sticky CUDA error surfaces as CULE_E_CUDA on a later call;
+ *   - per-environment runtime faults (JAM / unstable opcode, runaway frame) are data, not call
+ *     errors: the env reports done = 1 with reward 0 and an all-zero observation, is reset from
+ *     the cache, and the `faults` counter is incremented.
+ */
+#ifndef CULE_H
+#define CULE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CULE_OK 0
+#define CULE_E_INVAL (-1)    /* bad argument (null pointer, size, range, workspace too small) */
+#define CULE_E_ROM_SIZE (-2) /* ROM length not in {4096 (4K), 8192 (F8)}           */
+#define CULE_E_ROM_FAULT (-3)/* the reset-cache build hit a JAM or a runaway frame             */
+#define CULE_E_CUDA (-4)     /* CUDA launch / runtime failure                                  */
+#define CULE_E_CLOSED (-5)   /* use after cule_destroy                             */
+
+#define CULE_OBS_RAW 0    /* obs = u8[N][210][160] palette index (COLUxx >> 1) of the last frame */
+#define CULE_OBS_GRAY84 1 /* obs = u8[N][84][84] area84(max(gray(frame fs-1), gray(frame fs)))   */
+
+#define CULE_STATE_BYTES 256 /* packed per-env snapshot, layout in DESIGN.md §3 */
+#define CULE_FRAME_W 160
+#define CULE_FRAME_H 210
+
+typedef struct cule_env cule_env; /* opaque, owned by the library */
+
+typedef struct {
+  int32_t obs_mode;           /* CULE_OBS_RAW or CULE_OBS_GRAY84 (default GRAY84)            */
+  int32_t reset_cache_size;   /* K cached start states per ROM (default 30)       */
+  int32_t startup_frames;     /* NOOP frames after power-on (default 64)              */
+  int32_t max_random_frames;  /* R: + u_k in [0, R] extra NOOP frames (default 30)*/
+  int32_t max_episode_frames; /* done when an episode reaches this many frames; 0 = no cap   */
+  int32_t line_cap;           /* runaway-frame fault after this many scanlines (default 1024)*/
+  int32_t ystart;             /* frame-relative scanline of observation row 0 (default 34)   */
+  uint8_t score_addr;         /* RAM bus address ($80-$FE) of the BCD score high byte; low at +1 */
+  uint8_t term_addr;          /* done iff (RAM[term_addr] & term_mask) != 0 ($80-$FF)        */
+  uint8_t term_mask;
+  uint8_t reserved_;
+  uint64_t seed;              /* reset-cache construction seed (u_k draws)                   */
+  int64_t env_index_base;     /* global id of local env 0 (multi-GPU sharding)               */
+  const uint8_t* palette_rgb; /* HOST, 128 x (R,G,B) NTSC palette; read only during
+                                 cule_create; required for GRAY84 (gray LUT), ignored for RAW  */
+} cule_config;
+
+/* Fill *cfg with the defaults above (score $80/$81, terminal $82 bit 0, seed 0, base 0). */
+void cule_default_config(cule_config* cfg);
+
+/* Bytes of device workspace cule_create needs for (num_envs, n_roms, cfg).  0 on bad input. */
+size_t cule_workspace_bytes(int num_envs, int n_roms, const cule_config* cfg);
+
+/* Create a batch of num_envs environments.  Env with global id g = env_index_base + i runs
+ * ROM g % n_roms.  roms[r] / rom_lens[r] are HOST buffers (copied; may be freed afterwards);
+ * 1 <= n_roms <= 4; each length must be 4096 (4K) or 8192 (F8).  d_workspace (device,
+ * >= cule_workspace_bytes, 256-byte aligned) must outlive the handle.  Builds the reset cache
+ * on the device (synchronous: returns after the build, CULE_E_ROM_FAULT if any entry faulted).
+ * The handle uses the device current at the call.  Errors: CULE_E_INVAL, CULE_E_ROM_SIZE,
+ * CULE_E_ROM_FAULT, CULE_E_CUDA. */
+int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int num_envs,
+                int frameskip, const cule_config* cfg, void* d_workspace, size_t workspace_bytes,
+                cule_env** out);
+
+/* All envs <- cache[rom(g)][pick(seed, g, 0)] (pick = splitmix64 hash, DESIGN.md §2 R#22);
+ * bookkeeping and the per-GPU counters are zeroed.  d_obs (device, may be NULL) receives each
+ * env's cached observation in the layout of the obs mode.  Async on cuda_stream. */
+int cule_reset(cule_env* env, uint64_t seed, void* d_obs, void* cuda_stream);
+
+/* One step of every env: latch d_actions[i] (u8, ALE 18-action ids; >= 18 = NOOP), run
+ * frameskip frames, write d_obs (u8, layout per obs mode), d_rewards (i32, BCD score delta),
+ * d_dones (u8), then reset done envs from the cache.  All pointers are device pointers of
+ * N elements.  Async on cuda_stream. */
+int cule_step(cule_env* env, const uint8_t* d_actions, void* d_obs, int32_t* d_rewards,
+              uint8_t* d_dones, void* cuda_stream);
+
+/* Same as cule_step but with HOST buffers: copies h_actions in, steps, copies obs/rewards/
+ * dones out through the workspace's I/O staging area; synchronises cuda_stream before
+ * returning.  h_obs may be NULL (observations stay on the device). */
+int cule_step_host(cule_env* env, const uint8_t* h_actions, void* h_obs, int32_t* h_rewards,
+                   uint8_t* h_dones, void* cuda_stream);
+
+/* Copy the packed snapshots u8[N][256] to / from HOST memory.  Synchronous
+ * with respect to cuda_stream. */
+int cule_get_state(cule_env* env, uint8_t* h_states, void* cuda_stream);
+int cule_set_state(cule_env* env, const uint8_t* h_states, void* cuda_stream);
+
+/* Copy the per-GPU counters int64[4] = {frames, episodes finished, sum of finished episode
+ * returns, faults} to DEVICE memory d_counters4.  Async on cuda_stream. */
+int cule_counters(cule_env* env, int64_t* d_counters4, void* cuda_stream);
+
+/* Diagnostic entry for single-instruction parity tests: every env executes up to n_instr
+ * instructions (no rendering; a VSYNC rise ends the frame and stops that env), then the TIA
+ * is caught up to the CPU clock.  d_status (device i32[N], may be NULL) gets 0 = budget used,
+ * 1 = JAM/unstable opcode, 2 = runaway, 3 = frame ended.  Async on cuda_stream. */
+int cule_debug_exec(cule_env* env, int n_instr, int32_t* d_status, void* cuda_stream);
+
+/* Number of envs / frameskip / observation bytes per env of a handle. */
+int cule_num_envs(const cule_env* env);
+int cule_frameskip(const cule_env* env);
+size_t cule_obs_bytes(const cule_env* env);
+
+/* Release the handle (not the caller-owned workspace).  Using it afterwards is an error. */
+int cule_destroy(cule_env* env);
+
+const char* cule_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CULE_H */

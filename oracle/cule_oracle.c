@@ -808,9 +808,12 @@ static int run(Machine* m, int line_cap, long max_instr, int64_t* icount) {
       return 0;
     }
     int f = exec_one(m);
-    if (f) { m->fault = 1; if (icount) *icount += n; return 1; }
+    /* on a fault the TIA is still caught up to the CPU clock (R#26) */
+    if (f) { m->fault = 1; tia_catch_up(m, 3u * m->fc); if (icount) *icount += n; return 1; }
     n++;
-    if ((int)(m->fc / 76) >= line_cap) { m->fault = 2; if (icount) *icount += n; return 2; }
+    if ((int)(m->fc / 76) >= line_cap) {
+      m->fault = 2; tia_catch_up(m, 3u * m->fc); if (icount) *icount += n; return 2;
+    }
     if (m->vsync_rose) { end_frame(m); if (icount) *icount += n; return 3; }
   }
 }

@@ -1,0 +1,372 @@
+// cule.cu — libcule: the C-ABI boundary (include/cule.h) over the sm_100a kernels.
+//
+// Host code only marshals arguments, carves the caller-owned workspace and launches kernels;
+// every step of the emulation path runs on the device (kernels.cuh).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+
+#include "../../include/cule.h"
+#include "decode_table.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_live_mu;
+std::set<const void*> g_live;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t state, pack, staging, cstate, cobs, cscore, cstage, roms, decode, gray, counters, err,
+      io_act, io_obs, io_rew, io_done, total;
+};
+
+size_t obs_bytes_of(int mode) { return mode == CULE_OBS_RAW ? (size_t)cule::kFrameBytes : (size_t)cule::kObs84; }
+
+bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
+  if (N <= 0 || n_roms < 1 || n_roms > 4 || !c || c->reset_cache_size < 1) return false;
+  const size_t n = (size_t)N;
+  const size_t nk = (size_t)n_roms * (size_t)c->reset_cache_size;
+  const size_t ob = obs_bytes_of(c->obs_mode);
+  const bool gray = c->obs_mode == CULE_OBS_GRAY84;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+  L->state = take(256 * n);
+  L->pack = take(256 * n);
+  L->staging = take(gray ? n * cule::kFrameBytes : 0);
+  L->cstate = take(256 * nk);
+  L->cobs = take(nk * ob);
+  L->cscore = take(2 * nk);
+  L->cstage = take(gray ? nk * cule::kFrameBytes : 0);
+  L->roms = take(4 * 8192);
+  L->decode = take(1024);
+  L->gray = take(128);
+  L->counters = take(32);
+  L->err = take(16);
+  L->io_act = take(n);
+  L->io_obs = take(n * ob);
+  L->io_rew = take(4 * n);
+  L->io_done = take(n);
+  L->total = o;
+  return true;
+}
+
+}  // namespace
+
+struct cule_env {
+  cule_config cfg;
+  int N, fs, n_roms, device;
+  uint8_t* ws;
+  Layout L;
+  uint32_t rom_off[4];
+  uint32_t rom_bytes;
+  uint32_t f8_mask;
+  uint64_t pick_seed;
+  size_t smem;
+};
+
+static cule::Params base_params(const cule_env* e) {
+  cule::Params p;
+  std::memset(&p, 0, sizeof p);
+  p.state = e->ws + e->L.state;
+  p.N = (uint32_t)e->N;
+  p.staging = e->ws + e->L.staging;
+  p.roms = e->ws + e->L.roms;
+  p.rom_bytes = e->rom_bytes;
+  for (int r = 0; r < 4; ++r) p.rom_off[r] = e->rom_off[r];
+  p.f8_mask = e->f8_mask;
+  p.n_roms = (uint32_t)e->n_roms;
+  p.decode = reinterpret_cast<const uint32_t*>(e->ws + e->L.decode);
+  p.gray = e->ws + e->L.gray;
+  p.cache_state = e->ws + e->L.cstate;
+  p.cache_score = reinterpret_cast<const uint16_t*>(e->ws + e->L.cscore);
+  p.K = (uint32_t)e->cfg.reset_cache_size;
+  p.counters = reinterpret_cast<unsigned long long*>(e->ws + e->L.counters);
+  p.fs = (uint32_t)e->fs;
+  p.line_cap = (uint32_t)e->cfg.line_cap;
+  p.ystart = (uint32_t)e->cfg.ystart;
+  p.score_addr = e->cfg.score_addr;
+  p.term_addr = e->cfg.term_addr;
+  p.term_mask = e->cfg.term_mask;
+  p.max_episode_frames = (uint32_t)e->cfg.max_episode_frames;
+  p.pick_seed = e->pick_seed;
+  p.env_base = e->cfg.env_index_base;
+  p.startup_frames = (uint32_t)e->cfg.startup_frames;
+  p.max_random_frames = (uint32_t)e->cfg.max_random_frames;
+  p.cache_seed = e->cfg.seed;
+  p.cache_state_out = e->ws + e->L.cstate;
+  p.cache_obs_out = e->ws + e->L.cobs;
+  p.cache_score_out = reinterpret_cast<uint16_t*>(e->ws + e->L.cscore);
+  p.cache_staging = e->ws + e->L.cstage;
+  p.error_flag = reinterpret_cast<int32_t*>(e->ws + e->L.err);
+  return p;
+}
+
+static bool live(const cule_env* e) {
+  std::lock_guard<std::mutex> g(g_live_mu);
+  return e && g_live.count(e);
+}
+
+#define CHECK_LIVE(e) \
+  do { if (!live(e)) return fail(CULE_E_CLOSED, "invalid or destroyed cule_env handle"); } while (0)
+
+static int cuda_check(const char* what) {
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return fail(CULE_E_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+  return CULE_OK;
+}
+
+static constexpr int kBlock = 128;
+
+extern "C" {
+
+void cule_default_config(cule_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->obs_mode = CULE_OBS_GRAY84;
+  c->reset_cache_size = 30;
+  c->startup_frames = 64;
+  c->max_random_frames = 30;
+  c->max_episode_frames = 0;
+  c->line_cap = 1024;
+  c->ystart = 34;
+  c->score_addr = 0x80;
+  c->term_addr = 0x82;
+  c->term_mask = 0x01;
+  c->seed = 0;
+  c->env_index_base = 0;
+  c->palette_rgb = nullptr;
+}
+
+size_t cule_workspace_bytes(int num_envs, int n_roms, const cule_config* cfg) {
+  Layout L;
+  if (!compute_layout(num_envs, n_roms, cfg, &L)) return 0;
+  return L.total;
+}
+
+int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int num_envs,
+                int frameskip, const cule_config* cfg, void* d_workspace, size_t workspace_bytes,
+                cule_env** out) {
+  if (!out) return fail(CULE_E_INVAL, "out is NULL");
+  *out = nullptr;
+  if (!roms || !rom_lens || !cfg || !d_workspace) return fail(CULE_E_INVAL, "null argument");
+  if (n_roms < 1 || n_roms > 4) return fail(CULE_E_INVAL, "n_roms must be in [1, 4]");
+  if (num_envs <= 0) return fail(CULE_E_INVAL, "num_envs must be > 0");
+  if (frameskip < 1) return fail(CULE_E_INVAL, "frameskip must be >= 1");
+  if (cfg->obs_mode != CULE_OBS_RAW && cfg->obs_mode != CULE_OBS_GRAY84)
+    return fail(CULE_E_INVAL, "bad obs_mode");
+  if (cfg->reset_cache_size < 1 || cfg->startup_frames < 0 || cfg->max_random_frames < 0 ||
+      cfg->line_cap < 1 || cfg->ystart < 0 || cfg->ystart + cule::kFrameH > cfg->line_cap ||
+      cfg->max_episode_frames < 0)
+    return fail(CULE_E_INVAL, "bad config value");
+  if (cfg->score_addr < 0x80 || cfg->score_addr == 0xFF || cfg->term_addr < 0x80)
+    return fail(CULE_E_INVAL, "score/terminal addresses must be RAM bus addresses $80-$FF");
+  if (cfg->obs_mode == CULE_OBS_GRAY84 && !cfg->palette_rgb)
+    return fail(CULE_E_INVAL, "GRAY84 needs cfg->palette_rgb (384 bytes)");
+  if (((uintptr_t)d_workspace & 255) != 0) return fail(CULE_E_INVAL, "workspace must be 256-byte aligned");
+  for (int r = 0; r < n_roms; ++r) {
+    if (!roms[r]) return fail(CULE_E_INVAL, "null ROM");
+    if (rom_lens[r] != 4096 && rom_lens[r] != 8192)
+      return fail(CULE_E_ROM_SIZE, "ROM size must be 4096 (4K) or 8192 (F8), got " + std::to_string(rom_lens[r]));
+  }
+  Layout L;
+  compute_layout(num_envs, n_roms, cfg, &L);
+  if (workspace_bytes < L.total)
+    return fail(CULE_E_INVAL, "workspace too small: need " + std::to_string(L.total));
+
+  cule_env* e = new cule_env;
+  e->cfg = *cfg;
+  e->cfg.palette_rgb = nullptr;
+  e->N = num_envs;
+  e->fs = frameskip;
+  e->n_roms = n_roms;
+  cudaGetDevice(&e->device);
+  e->ws = static_cast<uint8_t*>(d_workspace);
+  e->L = L;
+  e->pick_seed = 0;
+  e->f8_mask = 0;
+  uint32_t off = 0;
+  for (int r = 0; r < 4; ++r) e->rom_off[r] = 0;
+  for (int r = 0; r < n_roms; ++r) {
+    e->rom_off[r] = off;
+    off += (uint32_t)rom_lens[r];
+    if (rom_lens[r] == 8192) e->f8_mask |= 1u << r;
+  }
+  e->rom_bytes = off;
+  e->smem = cule::smem_bytes(e->rom_bytes, kBlock);
+
+  // static inputs: ROM images, decode table, gray LUT (ITU-R 601 integer, half-up, §8(c).12)
+  uint8_t romimg[4 * 8192];
+  for (int r = 0; r < n_roms; ++r) std::memcpy(romimg + e->rom_off[r], roms[r], rom_lens[r]);
+  uint32_t table[256];
+  cule::build_decode_table(table);
+  uint8_t gray[128] = {0};
+  if (cfg->palette_rgb) {
+    for (int i = 0; i < 128; ++i) {
+      int R = cfg->palette_rgb[3 * i], G = cfg->palette_rgb[3 * i + 1], B = cfg->palette_rgb[3 * i + 2];
+      gray[i] = (uint8_t)((299 * R + 587 * G + 114 * B + 500) / 1000);
+    }
+  }
+  cudaMemcpy(e->ws + L.roms, romimg, e->rom_bytes, cudaMemcpyHostToDevice);
+  cudaMemcpy(e->ws + L.decode, table, sizeof table, cudaMemcpyHostToDevice);
+  cudaMemcpy(e->ws + L.gray, gray, sizeof gray, cudaMemcpyHostToDevice);
+  cudaMemset(e->ws + L.state, 0, 256 * (size_t)num_envs);
+  cudaMemset(e->ws + L.counters, 0, 32);
+  cudaMemset(e->ws + L.err, 0, 16);
+  int rc = cuda_check("workspace init");
+  if (rc) { delete e; return rc; }
+
+  const bool g = cfg->obs_mode == CULE_OBS_GRAY84;
+  cudaFuncSetAttribute(cule::step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  cudaFuncSetAttribute(cule::step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  cudaFuncSetAttribute(cule::cache_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  cudaFuncSetAttribute(cule::cache_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  cudaFuncSetAttribute(cule::debug_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+
+  // reset cache build: one thread per (rom, entry)
+  cule::Params p = base_params(e);
+  const uint32_t total = (uint32_t)n_roms * (uint32_t)cfg->reset_cache_size;
+  const uint32_t blocks = (total + kBlock - 1) / kBlock;
+  if (g) cule::cache_kernel<true><<<blocks, kBlock, e->smem>>>(p);
+  else cule::cache_kernel<false><<<blocks, kBlock, e->smem>>>(p);
+  rc = cuda_check("cache_kernel launch");
+  if (rc) { delete e; return rc; }
+  int32_t err_flag = 0;
+  if (cudaMemcpy(&err_flag, e->ws + L.err, sizeof err_flag, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    rc = cuda_check("cache_kernel");
+    delete e;
+    return rc ? rc : fail(CULE_E_CUDA, "cache build failed");
+  }
+  if (err_flag) {
+    delete e;
+    return fail(CULE_E_ROM_FAULT, "reset-cache build hit a JAM or runaway frame");
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    g_live.insert(e);
+  }
+  *out = e;
+  return CULE_OK;
+}
+
+int cule_reset(cule_env* e, uint64_t seed, void* d_obs, void* stream) {
+  CHECK_LIVE(e);
+  e->pick_seed = seed;
+  cule::Params p = base_params(e);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t blocks = ((uint32_t)e->N + 255) / 256;
+  cule::reset_kernel<<<blocks, 256, 0, s>>>(p, (uint32_t)obs_bytes_of(e->cfg.obs_mode),
+                                            static_cast<uint8_t*>(d_obs), e->ws + e->L.cobs);
+  cudaMemsetAsync(e->ws + e->L.counters, 0, 32, s);
+  return cuda_check("reset_kernel");
+}
+
+static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32_t* d_rewards,
+                       uint8_t* d_dones, cudaStream_t s) {
+  cule::Params p = base_params(e);
+  p.actions = d_actions;
+  p.obs = static_cast<uint8_t*>(d_obs);
+  p.rewards = d_rewards;
+  p.dones = d_dones;
+  const uint32_t blocks = ((uint32_t)e->N + kBlock - 1) / kBlock;
+  if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::step_kernel<true><<<blocks, kBlock, e->smem, s>>>(p);
+  else cule::step_kernel<false><<<blocks, kBlock, e->smem, s>>>(p);
+  return cuda_check("step_kernel");
+}
+
+int cule_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32_t* d_rewards,
+              uint8_t* d_dones, void* stream) {
+  CHECK_LIVE(e);
+  if (!d_actions || !d_obs || !d_rewards || !d_dones) return fail(CULE_E_INVAL, "null buffer");
+  return launch_step(e, d_actions, d_obs, d_rewards, d_dones, static_cast<cudaStream_t>(stream));
+}
+
+int cule_step_host(cule_env* e, const uint8_t* h_actions, void* h_obs, int32_t* h_rewards,
+                   uint8_t* h_dones, void* stream) {
+  CHECK_LIVE(e);
+  if (!h_actions || !h_rewards || !h_dones) return fail(CULE_E_INVAL, "null buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = (size_t)e->N, ob = obs_bytes_of(e->cfg.obs_mode);
+  uint8_t* act = e->ws + e->L.io_act;
+  uint8_t* obs = e->ws + e->L.io_obs;
+  int32_t* rew = reinterpret_cast<int32_t*>(e->ws + e->L.io_rew);
+  uint8_t* done = e->ws + e->L.io_done;
+  cudaMemcpyAsync(act, h_actions, n, cudaMemcpyHostToDevice, s);
+  int rc = launch_step(e, act, obs, rew, done, s);
+  if (rc) return rc;
+  if (h_obs) cudaMemcpyAsync(h_obs, obs, n * ob, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(h_rewards, rew, 4 * n, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(h_dones, done, n, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_check("cule_step_host");
+  return cuda_check("cule_step_host");
+}
+
+int cule_get_state(cule_env* e, uint8_t* h_states, void* stream) {
+  CHECK_LIVE(e);
+  if (!h_states) return fail(CULE_E_INVAL, "null buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = (size_t)e->N;
+  cule::pack_kernel<<<(unsigned)((n * 16 + 255) / 256), 256, 0, s>>>(e->ws + e->L.state, e->ws + e->L.pack, (uint32_t)n);
+  cudaMemcpyAsync(h_states, e->ws + e->L.pack, 256 * n, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  return cuda_check("cule_get_state");
+}
+
+int cule_set_state(cule_env* e, const uint8_t* h_states, void* stream) {
+  CHECK_LIVE(e);
+  if (!h_states) return fail(CULE_E_INVAL, "null buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = (size_t)e->N;
+  cudaMemcpyAsync(e->ws + e->L.pack, h_states, 256 * n, cudaMemcpyHostToDevice, s);
+  cule::unpack_kernel<<<(unsigned)((n * 16 + 255) / 256), 256, 0, s>>>(e->ws + e->L.state, e->ws + e->L.pack, (uint32_t)n);
+  cudaStreamSynchronize(s);
+  return cuda_check("cule_set_state");
+}
+
+int cule_counters(cule_env* e, int64_t* d_counters4, void* stream) {
+  CHECK_LIVE(e);
+  if (!d_counters4) return fail(CULE_E_INVAL, "null buffer");
+  cudaMemcpyAsync(d_counters4, e->ws + e->L.counters, 32, cudaMemcpyDeviceToDevice,
+                  static_cast<cudaStream_t>(stream));
+  return cuda_check("cule_counters");
+}
+
+int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
+  CHECK_LIVE(e);
+  if (n_instr < 0) return fail(CULE_E_INVAL, "n_instr must be >= 0");
+  cule::Params p = base_params(e);
+  p.debug_instr = n_instr;
+  p.debug_status = d_status;
+  const uint32_t blocks = ((uint32_t)e->N + kBlock - 1) / kBlock;
+  cule::debug_kernel<<<blocks, kBlock, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return cuda_check("debug_kernel");
+}
+
+int cule_num_envs(const cule_env* e) { return live(e) ? e->N : CULE_E_CLOSED; }
+int cule_frameskip(const cule_env* e) { return live(e) ? e->fs : CULE_E_CLOSED; }
+size_t cule_obs_bytes(const cule_env* e) { return live(e) ? obs_bytes_of(e->cfg.obs_mode) : 0; }
+
+int cule_destroy(cule_env* e) {
+  {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    if (!e || !g_live.count(e)) return fail(CULE_E_CLOSED, "invalid or destroyed cule_env handle");
+    g_live.erase(e);
+  }
+  delete e;
+  return CULE_OK;
+}
+
+const char* cule_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

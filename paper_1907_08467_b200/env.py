@@ -1,0 +1,134 @@
+"""`Env`: the Python face of libcule — batched Atari 2600 environments on one GPU.
+
+PyTorch supplies device memory (workspace, observation/reward/done buffers) and streams; the
+library does all of the work on the device ("CuLE comes with a python
+interface"; SPEC.md S:541-566 flat create/step/reset/close, preallocated reusable buffers).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .inputs import palette as _palette
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Env:
+    """N environments; env with global id g = env_index_base + i runs roms[g % len(roms)].
+
+    obs_mode: 'gray84' -> obs u8[N, 84, 84]; 'raw' -> obs u8[N, 210, 160] palette indices.
+    Output tensors are preallocated once and overwritten by every step.
+    """
+
+    def __init__(self, roms, num_envs: int, frameskip: int = 4, obs_mode: str = "gray84",
+                 seed: int = 0, device=None, env_index_base: int = 0, **cfg):
+        L = _lib.load()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        if self.device.type != "cuda":
+            raise ValueError("Env runs on a CUDA device only (no CPU fallback)")
+        roms = [bytes(r) for r in roms]
+        self.num_envs = int(num_envs)
+        self.frameskip = int(frameskip)
+        c = _lib.default_config()
+        c.obs_mode = _lib.CULE_OBS_GRAY84 if obs_mode == "gray84" else _lib.CULE_OBS_RAW
+        c.seed = seed
+        c.env_index_base = env_index_base
+        for k, v in cfg.items():
+            setattr(c, k, v)
+        self._pal = np.frombuffer(_palette.load_palette(), np.uint8).copy()
+        c.palette_rgb = self._pal.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+        self.cfg = c
+        self.obs_mode = obs_mode
+        with torch.cuda.device(self.device):
+            nbytes = L.cule_workspace_bytes(self.num_envs, len(roms), ctypes.byref(c))
+            if nbytes == 0:
+                raise _lib.CuleError(_lib.CULE_E_INVAL, "bad workspace request")
+            self._ws_raw = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+            base = self._ws_raw.data_ptr()
+            off = (-base) % 256
+            self._ws_ptr = base + off
+            self._roms = [np.frombuffer(r, np.uint8).copy() for r in roms]
+            arr = (ctypes.POINTER(ctypes.c_uint8) * len(roms))(
+                *[r.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)) for r in self._roms])
+            lens = (ctypes.c_size_t * len(roms))(*[len(r) for r in roms])
+            h = ctypes.c_void_p()
+            _lib.check(L.cule_create(arr, lens, len(roms), self.num_envs, self.frameskip,
+                                     ctypes.byref(c), ctypes.c_void_p(self._ws_ptr), nbytes,
+                                     ctypes.byref(h)))
+            self._h = h
+            shape = (84, 84) if obs_mode == "gray84" else (210, 160)
+            self.obs = torch.zeros((self.num_envs,) + shape, dtype=torch.uint8, device=self.device)
+            self.rewards = torch.zeros(self.num_envs, dtype=torch.int32, device=self.device)
+            self.dones = torch.zeros(self.num_envs, dtype=torch.uint8, device=self.device)
+            self._counters = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.obs_bytes = int(np.prod(shape))
+
+    # -- core calls ----------------------------------------------------------------------------
+    def reset(self, seed: int = 0, stream=None) -> torch.Tensor:
+        _lib.check(_lib.load().cule_reset(self._h, seed, ctypes.c_void_p(self.obs.data_ptr()),
+                                          ctypes.c_void_p(_stream_ptr(stream))))
+        return self.obs
+
+    def step(self, actions: torch.Tensor, stream=None):
+        if actions.dtype != torch.uint8 or actions.device != self.device or actions.numel() != self.num_envs:
+            raise ValueError("actions must be a uint8 tensor of N elements on the env's device")
+        actions = actions.contiguous()
+        _lib.check(_lib.load().cule_step(self._h, ctypes.c_void_p(actions.data_ptr()),
+                                         ctypes.c_void_p(self.obs.data_ptr()),
+                                         ctypes.c_void_p(self.rewards.data_ptr()),
+                                         ctypes.c_void_p(self.dones.data_ptr()),
+                                         ctypes.c_void_p(_stream_ptr(stream))))
+        return self.obs, self.rewards, self.dones
+
+    def step_host(self, h_actions: torch.Tensor, h_obs, h_rewards: torch.Tensor,
+                  h_dones: torch.Tensor, stream=None):
+        """Host-buffer step (pinned CPU tensors): copies in, steps, copies out, synchronises."""
+        _lib.check(_lib.load().cule_step_host(
+            self._h, ctypes.c_void_p(h_actions.data_ptr()),
+            ctypes.c_void_p(h_obs.data_ptr() if h_obs is not None else 0),
+            ctypes.c_void_p(h_rewards.data_ptr()), ctypes.c_void_p(h_dones.data_ptr()),
+            ctypes.c_void_p(_stream_ptr(stream))))
+
+    def get_state(self, stream=None) -> np.ndarray:
+        out = np.zeros((self.num_envs, _lib.STATE_BYTES), np.uint8)
+        _lib.check(_lib.load().cule_get_state(self._h, ctypes.c_void_p(out.ctypes.data),
+                                              ctypes.c_void_p(_stream_ptr(stream))))
+        return out
+
+    def set_state(self, states: np.ndarray, stream=None) -> None:
+        s = np.ascontiguousarray(states, dtype=np.uint8)
+        if s.shape != (self.num_envs, _lib.STATE_BYTES):
+            raise ValueError("states must be u8[N, 256]")
+        _lib.check(_lib.load().cule_set_state(self._h, ctypes.c_void_p(s.ctypes.data),
+                                              ctypes.c_void_p(_stream_ptr(stream))))
+
+    def counters(self, stream=None) -> torch.Tensor:
+        """int64[4] on the device: frames, episodes finished, sum of episode returns, faults."""
+        _lib.check(_lib.load().cule_counters(self._h, ctypes.c_void_p(self._counters.data_ptr()),
+                                             ctypes.c_void_p(_stream_ptr(stream))))
+        return self._counters
+
+    def debug_exec(self, n_instr: int, stream=None) -> torch.Tensor:
+        status = torch.zeros(self.num_envs, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.load().cule_debug_exec(self._h, n_instr, ctypes.c_void_p(status.data_ptr()),
+                                               ctypes.c_void_p(_stream_ptr(stream))))
+        return status
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            torch.cuda.synchronize(self.device)
+            _lib.check(_lib.load().cule_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

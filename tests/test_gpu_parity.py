@@ -1,0 +1,274 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle, bit-exact.
+
+Every comparison is element by element on the same seeded inputs: observations, rewards,
+dones and the full 256-byte per-env snapshot (SURVEY.md §8(c).14 "Batched == sequential").
+"""
+import numpy as np
+import pytest
+
+import helpers as H
+from paper_1907_08467_b200.inputs import games, micro
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1907_08467_b200 import build
+    build.build()
+    import oracle
+    oracle.build()
+
+
+def pair(roms, n, fs, mode="gray84", **cfg):
+    import oracle
+    from paper_1907_08467_b200 import Env
+    gpu = Env(roms, n, fs, obs_mode=mode, **cfg)
+    ref = oracle.OracleEnv(roms, n, fs, H.palette_rgb(), obs_mode=1 if mode == "gray84" else 0, **cfg)
+    return gpu, ref
+
+
+def assert_same_state(gs, rs, what=""):
+    if not (gs == rs).all():
+        bad = np.nonzero((gs != rs).any(1))[0]
+        i = int(bad[0])
+        cols = np.nonzero(gs[i] != rs[i])[0]
+        raise AssertionError(f"{what}: {len(bad)} envs differ; env {i} bytes {cols[:16].tolist()} "
+                             f"gpu {gs[i][cols[:16]].tolist()} oracle {rs[i][cols[:16]].tolist()}")
+
+
+def run_parity(gpu, ref, steps, seed=1234, reset_seed=0, check_every=1):
+    og = gpu.reset(reset_seed).cpu().numpy()
+    orf = ref.reset(reset_seed)
+    assert (og == orf).all(), "reset observations differ"
+    assert_same_state(gpu.get_state(), ref.get_state(), "after reset")
+    acts = H.random_actions(gpu.num_envs, steps, seed)
+    n_done = 0
+    for t in range(steps):
+        a = torch.from_numpy(acts[t]).to(gpu.device)
+        o, r, d = gpu.step(a)
+        o2, r2, d2 = ref.step(acts[t])
+        o, r, d = o.cpu().numpy(), r.cpu().numpy(), d.cpu().numpy()
+        assert (r == r2).all(), f"step {t}: rewards differ"
+        assert (d == d2).all(), f"step {t}: dones differ"
+        if not (o == o2).all():
+            bad = np.nonzero((o != o2).reshape(len(o), -1).any(1))[0]
+            raise AssertionError(f"step {t}: observations differ for envs {bad[:8].tolist()}")
+        if t % check_every == 0 or t == steps - 1:
+            assert_same_state(gpu.get_state(), ref.get_state(), f"step {t}")
+        n_done += int(d.sum())
+    c = gpu.counters().cpu().numpy()
+    assert (c == ref.counters()).all(), (c, ref.counters())
+    return n_done
+
+
+def test_cfg1_raw_16x100():
+    """SURVEY.md §7(b) minimum slice: R1, 16 envs, fs=1, RAW, 100 frames, everything compared."""
+    gpu, ref = pair([games.build_rom("R1")], 16, 1, "raw", reset_cache_size=30)
+    run_parity(gpu, ref, 100)
+
+
+@pytest.mark.parametrize("name", ["R1", "R2", "R3", "R4"])
+def test_gray84_fs4(name):
+    gpu, ref = pair([games.build_rom(name)], 200, 4, reset_cache_size=8)
+    run_parity(gpu, ref, 40, check_every=5)
+
+
+def test_mixed_roms_ragged():
+    roms = [games.build_rom(n) for n in ("R1", "R2", "R3", "R4")]
+    gpu, ref = pair(roms, 131, 4, reset_cache_size=6)
+    run_parity(gpu, ref, 30, check_every=10)
+
+
+def test_raw_fs4_and_fs2():
+    gpu, ref = pair([games.build_rom("R2")], 40, 4, "raw", reset_cache_size=4)
+    run_parity(gpu, ref, 20, check_every=4)
+    gpu, ref = pair([games.build_rom("R3")], 40, 2, "gray84", reset_cache_size=4)
+    run_parity(gpu, ref, 20, check_every=4)
+
+
+def test_episode_ends_and_resets():
+    # short episode cap forces done + reset-from-cache inside the window (cfg3 behaviour)
+    gpu, ref = pair([games.build_rom("R1"), games.build_rom("R3")], 96, 4,
+                    reset_cache_size=5, max_episode_frames=24)
+    n_done = run_parity(gpu, ref, 25, check_every=3)
+    assert n_done > 96
+
+
+@pytest.mark.parametrize("src", [micro.m17_score(), micro.m14_jam(100), micro.m15_no_vsync(100)])
+def test_micro_programs_env(src):
+    rom = micro.build(src)
+    gpu, ref = pair([rom, games.build_rom("R1")], 34, 4, reset_cache_size=3, max_random_frames=2)
+    og = gpu.reset(0)
+    ref.reset(0)
+    for t in range(40):
+        a = np.full(34, 1 if t % 3 else 0, np.uint8)
+        o, r, d = gpu.step(torch.from_numpy(a).cuda())
+        o2, r2, d2 = ref.step(a)
+        assert (r.cpu().numpy() == r2).all() and (d.cpu().numpy() == d2).all(), t
+        assert (o.cpu().numpy() == o2).all(), t
+        assert_same_state(gpu.get_state(), ref.get_state(), f"step {t}")
+    assert (gpu.counters().cpu().numpy() == ref.counters()).all()
+
+
+STATIC_CASES = [
+    dict(pokes=[(0x09, 0x1E), (0x08, 0x44), (0x0E, 0xA5), (0x0A, 1)]),
+    dict(pokes=[(0x06, 0x86), (0x1B, 0xC1), (0x04, 7)], positions=[(0x10, 20)], hmove=True),
+    dict(pokes=[(0x1B, 0xFF), (0x1F, 2), (0x0A, 0x35), (0x0F, 0xFF)],
+         positions=[(0x10, 20), (0x14, 21)], store_collisions=True),
+    dict(pokes=[(0x09, 0x1E), (0x20, 0x70)], positions=[(0x10, 3)], hmove_row0=True),
+    dict(pokes=[(0x1B, 0xFF), (0x1C, 0x81), (0x1D, 2), (0x1E, 2), (0x25, 1), (0x05, 0x33)],
+         positions=[(0x10, 12), (0x11, 14), (0x12, 13), (0x13, 30)], store_collisions=True),
+]
+
+
+@pytest.mark.parametrize("case", range(len(STATIC_CASES)))
+def test_static_frames_raw(case):
+    rom = micro.build(micro.static_frame(**STATIC_CASES[case]))
+    gpu, ref = pair([rom], 8, 1, "raw", reset_cache_size=2, max_random_frames=1)
+    run_parity(gpu, ref, 6)
+
+
+def _random_states(n, n_roms, rng):
+    """Valid random snapshots (canonical field ranges) for single-instruction
+    cross-checks."""
+    s = np.zeros((n, 256), np.uint8)
+    s[:, 0:4] = rng.integers(0, 256, (n, 4))
+    s[:, 4] = (rng.integers(0, 256, n) & ~0x10) | 0x20
+    rom_id = rng.integers(0, n_roms, n)
+    s[:, 61] = rom_id
+    s[:, 5] = np.where(rom_id >= 2, rng.integers(0, 2, n), 0)         # ROMs 2,3 are F8
+    pcs = np.where(rng.random(n) < 0.9, rng.integers(0xF000, 0x10000, n),
+                   rng.integers(0x80, 0x100, n))
+    pcs = np.where(rng.random(n) < 0.02, rng.integers(0, 0x10000, n), pcs)
+    s[:, 6] = pcs & 0xFF
+    s[:, 7] = pcs >> 8
+    fc = rng.integers(0, 76 * 300, n)
+    s[:, 8:12] = fc.astype("<u4").view(np.uint8).reshape(n, 4)
+    tS = rng.choice([0, 3, 6, 10], n)
+    tV = rng.integers(0, 256, n)
+    e = rng.integers(0, (tV.astype(np.int64) << tS) + 300)
+    s[:, 12:16] = (fc - e).astype("<i4").view(np.uint8).reshape(n, 4)
+    s[:, 16] = tV
+    s[:, 17] = tS
+    s[:, 18] = rng.integers(0, 256, n)
+    s[:, 19] = rng.choice([0, 0x80], n)
+    coll = rng.integers(0, 1 << 16, n) & ~(1 << 13)
+    s[:, 20] = coll & 0xFF
+    s[:, 21] = coll >> 8
+    comb = np.where(rng.random(n) < 0.5, -1, rng.integers(0, 300, n))
+    s[:, 22:24] = comb.astype("<i2").view(np.uint8).reshape(n, 2)
+    for off in (24, 25, 33, 34, 42, 43, 44, 45, 51, 52, 53, 54, 55):
+        s[:, off] = rng.integers(0, 2, n)
+    for off in (26, 27, 28, 29, 30, 31, 32, 35, 36, 37, 38, 39, 40, 41):
+        s[:, off] = rng.integers(0, 256, n)
+    for off in (46, 47, 48, 49, 50):
+        s[:, off] = rng.integers(0, 16, n)
+    for off in range(56, 61):
+        s[:, off] = rng.integers(0, 160, n)
+    s[:, 64:192] = rng.integers(0, 256, (n, 128))
+    return s
+
+
+@pytest.mark.parametrize("n_instr", [1, 3, 40])
+def test_random_instructions(n_instr):
+    """>= 1e5 random (opcode, registers, memory) cases through the debug entry of the kernel
+    against the oracle's single-instruction execution."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    rng = np.random.default_rng(100 + n_instr)
+    roms = [rng.integers(0, 256, 4096, dtype=np.uint8).tobytes() for _ in range(2)] + \
+           [rng.integers(0, 256, 8192, dtype=np.uint8).tobytes() for _ in range(2)]
+    n = 100_000 if n_instr == 1 else 20_000
+    # RAW mode: no palette needed; only the debug entry is used (K=1 cache, 0 frames)
+    gpu = Env(roms, n, 1, obs_mode="raw", reset_cache_size=1, startup_frames=0, max_random_frames=0)
+    st = _random_states(n, 4, rng)
+    gpu.set_state(st)
+    status = gpu.debug_exec(n_instr).cpu().numpy()
+    got = gpu.get_state()
+    bad = []
+    for i in range(n):
+        s = st[i].copy()
+        r, _ = oracle.exec_instr(roms[st[i, 61]], s, n_instr)
+        if r != status[i] or not (s == got[i]).all():
+            bad.append(i)
+            if len(bad) > 5:
+                break
+    if bad:
+        i = bad[0]
+        s = st[i].copy()
+        r, _ = oracle.exec_instr(roms[st[i, 61]], s, n_instr)
+        cols = np.nonzero(s != got[i])[0]
+        op = roms[st[i, 61]][(int(st[i, 5]) << 12) + (H.pc(st[i]) & 0xFFF)] if H.pc(st[i]) & 0x1000 else None
+        raise AssertionError(f"{len(bad)}+ mismatches; env {i} op {op} pc {H.pc(st[i]):04x} status "
+                             f"gpu {status[i]} oracle {r}; bytes {cols.tolist()[:12]} gpu "
+                             f"{got[i][cols].tolist()[:12]} oracle {s[cols].tolist()[:12]}")
+
+
+def test_set_state_windowed_parity():
+    """Late, decorrelated states: run the oracle 30 steps, load its snapshots into the GPU, and
+    compare 10 more steps (SURVEY.md §8(d) windowed parity)."""
+    gpu, ref = pair([games.build_rom("R1"), games.build_rom("R2")], 64, 4, reset_cache_size=5)
+    gpu.reset(3)
+    ref.reset(3)
+    acts = H.random_actions(64, 40, 77)
+    for t in range(30):
+        ref.step(acts[t])
+    gpu.set_state(ref.get_state())
+    assert_same_state(gpu.get_state(), ref.get_state(), "set_state round trip")
+    for t in range(30, 40):
+        o, r, d = gpu.step(torch.from_numpy(acts[t]).cuda())
+        o2, r2, d2 = ref.step(acts[t])
+        assert (o.cpu().numpy() == o2).all() and (r.cpu().numpy() == r2).all()
+        assert_same_state(gpu.get_state(), ref.get_state(), f"step {t}")
+
+
+def test_num_envs_and_step_host_equivalence():
+    from paper_1907_08467_b200 import Env
+    rom = games.build_rom("R1")
+    big = Env([rom], 300, 4, reset_cache_size=6)
+    small = Env([rom], 20, 4, reset_cache_size=6)
+    host = Env([rom], 20, 4, reset_cache_size=6)
+    big.reset(9)
+    small.reset(9)
+    host.reset(9)
+    acts = H.random_actions(300, 15, 5)
+    h_act = torch.zeros(20, dtype=torch.uint8).pin_memory()
+    h_obs = torch.zeros((20, 84, 84), dtype=torch.uint8).pin_memory()
+    h_rew = torch.zeros(20, dtype=torch.int32).pin_memory()
+    h_done = torch.zeros(20, dtype=torch.uint8).pin_memory()
+    for t in range(15):
+        ob, rb, db = big.step(torch.from_numpy(acts[t]).cuda())
+        os_, rs, ds = small.step(torch.from_numpy(acts[t, :20]).cuda())
+        h_act.copy_(torch.from_numpy(acts[t, :20]))
+        host.step_host(h_act, h_obs, h_rew, h_done)
+        assert (ob[:20] == os_).all() and (rb[:20] == rs).all() and (db[:20] == ds).all()
+        assert (h_obs == os_.cpu()).all() and (h_rew == rs.cpu()).all() and (h_done == ds.cpu()).all()
+    assert (big.get_state()[:20] == small.get_state()).all()
+
+
+def test_sampled_parity_at_cfg2_size():
+    """cfg2 at full size (4096 envs, R1, fs=4, GRAY84, default K=30) in the bench's launch
+    configuration; 48 sampled envs replayed one by one in the oracle."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    rom = games.build_rom("R1")
+    N, steps = 4096, 12
+    gpu = Env([rom], N, 4)
+    gpu.reset(0)
+    acts = H.random_actions(N, steps, 1234)
+    sample = np.unique(np.concatenate([np.arange(0, 16), np.arange(N - 8, N),
+                                       np.random.default_rng(0).integers(0, N, 24)]))
+    ref = oracle.OracleEnv([rom], len(sample), 4, H.palette_rgb())
+    ref.set_env_ids(sample)
+    ref.reset(0)
+    for t in range(steps):
+        o, r, d = gpu.step(torch.from_numpy(acts[t]).cuda())
+        o2, r2, d2 = ref.step(acts[t][sample])
+        assert (o.cpu().numpy()[sample] == o2).all() and (r.cpu().numpy()[sample] == r2).all()
+        assert (d.cpu().numpy()[sample] == d2).all()
+    assert_same_state(gpu.get_state()[sample], ref.get_state(), "cfg2 sample")
