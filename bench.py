@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark: emulated (raw) Atari frames per second on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--envs E] [--config cfg2|cfg3|cfg4]
+    python bench.py --impl reference ...     # the CPU oracle on the host cores (reference arm)
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Default workload (N=1): BASELINE.json configs[1] = cfg2: 4096 envs of the generated 4 KB
+playfield ROM R1, frameskip 4, 84x84 grayscale max-pooled observations, random actions
+(P:318-320 emulation-only load), reset-from-cache on done.  One step = one cule_step over all
+envs (a0..a8 of SURVEY.md §8(a)).  Raw frames = envs x frameskip x steps.
+
+Multi-GPU: one process per GPU, env slice [rank*E, (rank+1)*E) via env_index_base (weak
+scaling); the only collective is one NCCL all_reduce of the int64[4] counters after timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (rom names, envs per GPU, frameskip, obs mode, description)
+    "cfg2": (["R1"], 4096, 4, "gray84", "cfg2: 4096 envs, generated 4 KB ROM R1, fs=4, GRAY84"),
+    "cfg3": (["R2"], 16384, 4, "gray84", "cfg3: 16384 envs, F8 ROM R2, fs=4, GRAY84, reset-from-cache"),
+    "cfg4": (["R1", "R2", "R3", "R4"], 32768, 4, "gray84", "cfg4: 32768 envs, R1-R4 interleaved, fs=4, GRAY84"),
+}
+
+# SASS thread-instructions the step kernel executes per raw frame on cfg2 (measured with
+# ncu smsp__thread_inst_executed.sum; profiles/ holds the capture).  Used for the issue roof.
+INST_PER_FRAME = {"cfg2": None, "cfg3": None, "cfg4": None}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--impl", default="cule", choices=["cule", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-envs", type=int, default=16)
+    ap.add_argument("--cpu-sample-steps", type=int, default=12)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in open(self.path):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm = float(parts[1].split()[0])
+                mx = float(parts[2].split()[0])
+            except ValueError:
+                continue
+            sms.append(sm)
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle as it stands, on the host cores
+# ---------------------------------------------------------------------------------------------
+def _oracle_worker(args):
+    rom_names, n_envs, fs, mode, base, steps, warmup, seed = args
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import oracle
+    from paper_1907_08467_b200.inputs import games, palette
+    roms = [games.build_rom(n) for n in rom_names]
+    env = oracle.OracleEnv(roms, n_envs, fs, palette.load_palette(), obs_mode=1 if mode == "gray84" else 0,
+                           env_index_base=base)
+    env.reset(0)
+    rng = np.random.default_rng(seed)
+    for _ in range(warmup):
+        env.step(rng.integers(0, 18, n_envs, dtype=np.uint8))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        env.step(rng.integers(0, 18, n_envs, dtype=np.uint8))
+    dt = time.perf_counter() - t0
+    return n_envs * fs * steps, dt
+
+
+def oracle_fps(rom_names, fs, mode, envs_per_proc, steps, warmup, procs):
+    import multiprocessing as mp
+    jobs = [(rom_names, envs_per_proc, fs, mode, 1_000_000 + k * envs_per_proc, steps, warmup, 1234 + k)
+            for k in range(procs)]
+    t0 = time.perf_counter()
+    if procs == 1:
+        res = [_oracle_worker(jobs[0])]
+    else:
+        with mp.get_context("spawn").Pool(procs) as pool:
+            res = pool.map(_oracle_worker, jobs)
+    wall = time.perf_counter() - t0
+    frames = sum(r[0] for r in res)
+    per_proc_time = max(r[1] for r in res)
+    return frames / per_proc_time, frames, per_proc_time, wall
+
+
+def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written), else the profiling guide's
+    fallback (6.65 TB/s, 1965 MHz)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return {"hbm_gbs": float(m["hbm_gbs"]), "sm_max_mhz": float(m.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    rom_names, envs, fs, mode, desc = CONFIGS[args.config]
+    if args.envs:
+        envs = args.envs
+    if rank != 0:
+        return
+    cores = host_cores()
+    procs = max(1, min(cores, 64))
+    # each timed oracle step runs a bounded sample of the workload: `procs` processes x 4 envs
+    fps, frames, t, wall = oracle_fps(rom_names, fs, mode, 4, args.steps, args.warmup, procs)
+    sample = (f"{procs} oracle processes x 4 envs (global ids >= 1e6) of {desc}; "
+              f"{args.warmup} warm-up + {args.steps} timed steps each")
+    line = {
+        "impl": "reference", "metric": "emulated frames/sec", "value": fps, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * t / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": desc, "envs_per_gpu": envs, "frameskip": fs, "obs": mode},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": procs, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+# the CUDA arm
+# ---------------------------------------------------------------------------------------------
+def run_cule(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1907_08467_b200 import Env, build
+    from paper_1907_08467_b200.inputs import games
+
+    build.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    rom_names, envs, fs, mode, desc = CONFIGS[args.config]
+    if args.envs:
+        envs = args.envs
+    roms = [games.build_rom(n) for n in rom_names]
+    env = Env(roms, envs, fs, obs_mode=mode, env_index_base=rank * envs, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    env.reset(0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    W, K = args.warmup, args.steps
+    acts = torch.randint(0, 18, (W + K, envs), generator=gen, device=dev, dtype=torch.uint8)
+    for t in range(W):
+        env.step(acts[t])
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev0.record(stream)
+    for t in range(W, W + K):
+        env.step(acts[t])
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    counters = env.counters().clone()
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
+    ms_max = float(ms_t.item())
+    frames_total = envs * world * fs * K
+    fps = frames_total / (ms_max / 1000.0)
+
+    # e2e through the C-ABI with pinned HOST buffers: H2D actions, step, D2H obs/rewards/dones
+    ob = env.obs_bytes
+    h_act = torch.zeros(envs, dtype=torch.uint8).pin_memory()
+    h_obs = torch.zeros((envs, ob), dtype=torch.uint8).pin_memory()
+    h_rew = torch.zeros(envs, dtype=torch.int32).pin_memory()
+    h_done = torch.zeros(envs, dtype=torch.uint8).pin_memory()
+    hgen = torch.Generator()
+    hgen.manual_seed(4321 + rank)
+    host_acts = torch.randint(0, 18, (args.e2e_steps + 3, envs), generator=hgen, dtype=torch.uint8)
+    for t in range(3):
+        h_act.copy_(host_acts[t])
+        env.step_host(h_act, h_obs, h_rew, h_done)
+    if world > 1:
+        dist.barrier()
+    e0 = time.perf_counter()
+    for t in range(args.e2e_steps):
+        h_act.copy_(host_acts[t])
+        env.step_host(h_act, h_obs, h_rew, h_done)
+    e_dt = time.perf_counter() - e0
+    e_t = torch.tensor([e_dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+    e2e_fps = envs * world * fs * args.e2e_steps / float(e_t.item())
+
+    if rank != 0:
+        return
+    # roofline of the dominant (only) kernel: step_kernel, one launch per step
+    pk = peaks()
+    launch_s = ms_max / 1000.0 / K
+    alg_bytes_per_env = 208 * 2 + 1 + 4 + 1 + (7056 if mode == "gray84" else 33600)
+    alg_bytes = alg_bytes_per_env * envs
+    hbm_gbs = alg_bytes / launch_s / 1e9
+    sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+    issue_peak = 148 * 4 * 32 * pk["sm_max_mhz"] * 1e6 / 1e12  # T lane-instr/s at max clock
+    ipf = INST_PER_FRAME.get(args.config)
+    roof = {"bound": "alu", "unit": "Tinst/s", "peak": issue_peak,
+            "achieved": (ipf * envs * fs / launch_s / 1e12) if ipf else None,
+            "traffic": None,
+            "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk["hbm_gbs"], "frac": hbm_gbs / pk["hbm_gbs"],
+                    "alg_bytes_per_launch": alg_bytes},
+            "peak_source": pk["source"]}
+    roof["frac"] = roof["achieved"] / issue_peak if roof["achieved"] else None
+    line = {
+        "metric": "emulated frames/sec", "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": desc, "envs_per_gpu": envs, "frameskip": fs, "obs": mode,
+                   "actions": "uniform random over 18, torch cuda generator seed 1234+rank",
+                   "l2": "per-step working set > 126 MB L2 (staging frames " +
+                         f"{envs * 33600 / 1e6:.0f} MB + obs + state)",
+                   "parallelism": f"dp{world} (env shards)"},
+        "fps_per_env": fps / (envs * world),
+        "training_frames_per_s": fps / 4,
+        "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": envs,
+                "d2h_bytes_per_step": envs * (ob + 4 + 1)},
+        "gpu_launches": K,
+        "roofline": roof,
+        "clocks": clk,
+        "counters": {"frames": int(counters[0]), "episodes": int(counters[1]),
+                     "return_sum": int(counters[2]), "faults": int(counters[3])},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        cores = host_cores()
+        procs = max(1, min(cores, 64))
+        cfps, frames, t, wall = oracle_fps(rom_names, fs, mode, args.cpu_sample_envs,
+                                           args.cpu_sample_steps, 2, procs)
+        line["cpu_baseline"] = {"value": cfps, "unit": "frames/s", "cores": procs, "kind": "oracle",
+                                "sample": f"{procs} processes x {args.cpu_sample_envs} envs x "
+                                          f"{args.cpu_sample_steps} steps of {desc} ({frames} frames, "
+                                          f"{t:.1f} s)", "cpu": cpu_model()}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        pass
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        run_cule(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
