@@ -1,237 +1,318 @@
-// cpu.cuh — 6502 instruction execution and the frame loop on top of emu.cuh.
+// cpu.cuh — the 6502/6507 + RIOT + bus of one environment, registers-resident.
 //
-// One instruction = (A) opcode/operand fetches and pointer reads, which fix the cycle count n;
-// (B) the instruction's end T = 3(fc+n) colour clocks; (C) data read, data write and stack
-// accesses, all sampling at T (DESIGN.md §2 R#4; SURVEY.md §8(c).4 "bus timing model").
-// The TIA is only caught up when an access touches it (or the frame ends).
+// One instruction (DESIGN.md §2 R#4): (A) opcode/operand fetches and pointer reads fix the
+// cycle count n; (B) the instruction ends at T = 3(fc+n) colour clocks; (C) data read, data
+// write and stack accesses all sample at T.  Ordinary instructions run through one branch-free
+// micro-coded datapath (decode_table.h); the data read of RAM or ROM is a single shared-memory
+// load whose address is selected arithmetically, so only TIA/RIOT/bank-switch accesses, stack
+// and control instructions, and decimal arithmetic leave the common path.
 #pragma once
-#include "emu.cuh"
+#include "decode_table.h"
+#include "tia.cuh"
 
 namespace cule {
 
-enum RunStatus : int32_t { RUN_BUDGET = 0, RUN_JAM = 1, RUN_RUNAWAY = 2, RUN_FRAME = 3 };
+enum Event : uint32_t { EV_NONE = 0, EV_LOGFULL = 1, EV_FRAME = 2, EV_FAULT = 3 };
 
-template <bool kGray>
-__device__ __forceinline__ uint32_t exec_one(Machine& m, bool& jam) {
-  m.now = m.fc;
-  m.wsync_req = 0;
-  m.vsync_rose = 0;
-  const uint32_t op = m.fetch<kGray>();
-  const uint32_t d = m.sm->decode[op];
-  const uint32_t mode = d & 0xFu;
-  const uint32_t oper = (d >> 4) & 0x7Fu;
-  uint32_t n = (d >> 11) & 0xFu;
-  if (oper == OP_JAM) { jam = true; return 0; }
-
-  // ---- phase A: effective address -------------------------------------------------------
-  uint32_t ea = 0, v = 0;
-  switch (mode) {
-    case AM_IMM: v = m.fetch<kGray>(); break;
-    case AM_ZP: ea = m.fetch<kGray>(); break;
-    case AM_ZPX: ea = (m.fetch<kGray>() + m.X) & 0xFFu; break;
-    case AM_ZPY: ea = (m.fetch<kGray>() + m.Y) & 0xFFu; break;
-    case AM_ABS: case AM_IND: case AM_ABSX: case AM_ABSY: {
-      uint32_t lo = m.fetch<kGray>();
-      uint32_t hi = m.fetch<kGray>();
-      uint32_t base = lo | (hi << 8);
-      if (mode == AM_ABS) { ea = base; break; }
-      if (mode == AM_IND) {
-        uint32_t tl = m.rd<kGray, true>(base);
-        uint32_t th = m.rd<kGray, true>((base & 0xFF00u) | ((base + 1) & 0xFFu));
-        ea = tl | (th << 8);
-        break;
-      }
-      ea = (base + (mode == AM_ABSX ? m.X : m.Y)) & 0xFFFFu;
-      if ((d >> 15) & 1u) n += ((ea ^ base) >> 8) & 1u ? 1u : 0u;
-    } break;
-    case AM_INDX: {
-      uint32_t p = (m.fetch<kGray>() + m.X) & 0xFFu;
-      uint32_t lo = m.rd<kGray, true>(p);
-      uint32_t hi = m.rd<kGray, true>((p + 1) & 0xFFu);
-      ea = lo | (hi << 8);
-    } break;
-    case AM_INDY: {
-      uint32_t p = m.fetch<kGray>();
-      uint32_t lo = m.rd<kGray, true>(p);
-      uint32_t hi = m.rd<kGray, true>((p + 1) & 0xFFu);
-      uint32_t base = lo | (hi << 8);
-      ea = (base + m.Y) & 0xFFFFu;
-      if ((d >> 15) & 1u) n += ((ea ^ base) >> 8) & 1u ? 1u : 0u;
-    } break;
-    case AM_REL: {
-      uint32_t off = m.fetch<kGray>();
-      uint32_t sel = (d >> 17) & 3u;
-      uint32_t flag = sel == 0 ? (m.nreg >> 7) & 1u
-                    : sel == 1 ? m.fV
-                    : sel == 2 ? m.fC
-                               : ((m.zreg & 0xFFu) == 0 ? 1u : 0u);
-      if (flag == ((d >> 19) & 1u)) {
-        uint32_t tgt = (m.PC + (uint32_t)(int32_t)(int8_t)off) & 0xFFFFu;
-        n += 1u + (((tgt ^ m.PC) >> 8) & 1u ? 1u : 0u);
-        m.PC = tgt;
-      }
-    } break;
-    default: break;  // implied / accumulator
-  }
-
-  // ---- phase B/C: accesses at the instruction's end -------------------------------------
-  m.now = m.fc + n;
-  if ((d >> 16) & 1u) v = m.rd<kGray, false>(ea);
-
-  switch (oper) {
-    case OP_LDA: m.A = v; m.nz(v); break;
-    case OP_LDX: m.X = v; m.nz(v); break;
-    case OP_LDY: m.Y = v; m.nz(v); break;
-    case OP_LAX: m.A = m.X = v; m.nz(v); break;
-    case OP_STA: m.wr<kGray>(ea, m.A); break;
-    case OP_STX: m.wr<kGray>(ea, m.X); break;
-    case OP_STY: m.wr<kGray>(ea, m.Y); break;
-    case OP_SAX: m.wr<kGray>(ea, m.A & m.X); break;
-    case OP_ORA: m.A |= v; m.nz(m.A); break;
-    case OP_AND: m.A &= v; m.nz(m.A); break;
-    case OP_EOR: m.A ^= v; m.nz(m.A); break;
-    case OP_ADC: m.adc(v); break;
-    case OP_SBC: m.sbc(v); break;
-    case OP_CMP: m.cmp(m.A, v); break;
-    case OP_CPX: m.cmp(m.X, v); break;
-    case OP_CPY: m.cmp(m.Y, v); break;
-    case OP_BIT: m.nreg = v; m.fV = (v >> 6) & 1u; m.zreg = m.A & v; break;
-    case OP_ASL: case OP_LSR: case OP_ROL: case OP_ROR: case OP_INC: case OP_DEC:
-    case OP_SLO: case OP_RLA: case OP_SRE: case OP_RRA: case OP_DCP: case OP_ISB: {
-      const bool acc = mode == AM_ACC;
-      uint32_t x = acc ? m.A : v;
-      uint32_t r;
-      switch (oper) {
-        case OP_ASL: case OP_SLO: m.fC = x >> 7; r = (x << 1) & 0xFFu; break;
-        case OP_LSR: case OP_SRE: m.fC = x & 1u; r = x >> 1; break;
-        case OP_ROL: case OP_RLA: r = ((x << 1) | m.fC) & 0xFFu; m.fC = x >> 7; break;
-        case OP_ROR: case OP_RRA: r = (x >> 1) | (m.fC << 7); m.fC = x & 1u; break;
-        case OP_INC: case OP_ISB: r = (x + 1) & 0xFFu; break;
-        default: r = (x - 1) & 0xFFu; break;  // DEC, DCP
-      }
-      switch (oper) {
-        case OP_SLO: m.A |= r; m.nz(m.A); break;
-        case OP_RLA: m.A &= r; m.nz(m.A); break;
-        case OP_SRE: m.A ^= r; m.nz(m.A); break;
-        case OP_RRA: m.adc(r); break;
-        case OP_DCP: m.cmp(m.A, r); break;
-        case OP_ISB: m.sbc(r); break;
-        default: m.nz(r); break;
-      }
-      if (acc) m.A = r; else m.wr<kGray>(ea, r);
-    } break;
-    case OP_ANC: m.A &= v; m.nz(m.A); m.fC = m.A >> 7; break;
-    case OP_ALR: { uint32_t t = m.A & v; m.fC = t & 1u; m.A = t >> 1; m.nz(m.A); } break;
-    case OP_ARR: {
-      uint32_t t = m.A & v;
-      m.A = (t >> 1) | (m.fC << 7);
-      m.nz(m.A);
-      m.fC = (m.A >> 6) & 1u;
-      m.fV = ((m.A >> 6) ^ (m.A >> 5)) & 1u;
-    } break;
-    case OP_SBX: { uint32_t t = m.A & m.X; m.fC = t >= v ? 1u : 0u; m.X = (t - v) & 0xFFu; m.nz(m.X); } break;
-    case OP_NOP: break;
-    case OP_INX: m.X = (m.X + 1) & 0xFFu; m.nz(m.X); break;
-    case OP_INY: m.Y = (m.Y + 1) & 0xFFu; m.nz(m.Y); break;
-    case OP_DEX: m.X = (m.X - 1) & 0xFFu; m.nz(m.X); break;
-    case OP_DEY: m.Y = (m.Y - 1) & 0xFFu; m.nz(m.Y); break;
-    case OP_TAX: m.X = m.A; m.nz(m.X); break;
-    case OP_TAY: m.Y = m.A; m.nz(m.Y); break;
-    case OP_TXA: m.A = m.X; m.nz(m.A); break;
-    case OP_TYA: m.A = m.Y; m.nz(m.A); break;
-    case OP_TSX: m.X = m.SP; m.nz(m.X); break;
-    case OP_TXS: m.SP = m.X; break;
-    case OP_CLC: m.fC = 0; break;
-    case OP_SEC: m.fC = 1; break;
-    case OP_CLI: m.fI = 0; break;
-    case OP_SEI: m.fI = 1; break;
-    case OP_CLV: m.fV = 0; break;
-    case OP_CLD: m.fD = 0; break;
-    case OP_SED: m.fD = 1; break;
-    case OP_PHA: m.push<kGray>(m.A); break;
-    case OP_PHP: m.push<kGray>(m.getP() | 0x30u); break;
-    case OP_PLA: m.A = m.pull<kGray>(); m.nz(m.A); break;
-    case OP_PLP: m.setP(m.pull<kGray>()); break;
-    case OP_JMP: m.PC = ea; break;
-    case OP_JSR: {
-      uint32_t ret = (m.PC - 1) & 0xFFFFu;  // address of the JSR's last byte
-      m.push<kGray>(ret >> 8);
-      m.push<kGray>(ret & 0xFFu);
-      m.PC = ea;
-    } break;
-    case OP_RTS: {
-      uint32_t lo = m.pull<kGray>();
-      uint32_t hi = m.pull<kGray>();
-      m.PC = ((lo | (hi << 8)) + 1) & 0xFFFFu;
-    } break;
-    case OP_RTI: {
-      m.setP(m.pull<kGray>());
-      uint32_t lo = m.pull<kGray>();
-      uint32_t hi = m.pull<kGray>();
-      m.PC = lo | (hi << 8);
-    } break;
-    case OP_BRK: {
-      uint32_t ret = (m.PC + 1) & 0xFFFFu;
-      m.push<kGray>(ret >> 8);
-      m.push<kGray>(ret & 0xFFu);
-      m.push<kGray>(m.getP() | 0x30u);
-      m.fI = 1;
-      uint32_t lo = m.rd<kGray, false>(0x1FFEu);
-      uint32_t hi = m.rd<kGray, false>(0x1FFFu);
-      m.PC = lo | (hi << 8);
-    } break;
-    default: break;  // OP_BRANCH handled in phase A
-  }
-  return n;
+// out-of-line so the rare collision-read path does not bloat the hot loop; scalar arguments
+// only, so no caller state is forced into local memory
+__device__ __noinline__ uint32_t coll_read_flush(uint32_t* tw, uint32_t* pw, const uint32_t* lg, uint32_t s,
+                                                 uint32_t n, uint32_t t, uint32_t ystart, const uint8_t* gray) {
+  flush_lane(tw, pw, lg, s, n, true, t, ystart, gray);
+  return tw[7 * s] >> 16;
 }
 
-// End the frame at the VSYNC edge: finish the TIA, rebase clocks to the VSYNC line, canonical
-// timer stamp (DESIGN.md §2 R#6, R#24).
-template <bool kGray>
-__device__ __forceinline__ void end_frame(Machine& m) {
-  m.catch_up<kGray>(3u * m.fc);
-  uint32_t L = m.fc / 76u;
-  m.last_lines = L;
-  m.fc -= 76u * L;
-  m.tW -= (int32_t)(76u * L);
-  m.t_tia -= 228u * L;
-  m.t_phaseA = m.t_tia;
-  int32_t cl = m.comb_line - (int32_t)L;
-  m.comb_line = cl < 0 ? -1 : cl;
-  int32_t e = (int32_t)m.fc - m.tW;
-  int32_t VI = (int32_t)(m.tV << m.tS);
-  if (e > VI) m.tW = (int32_t)m.fc - (VI + 1 + ((e - VI - 1) & 0xFF));
-}
+struct Ctx {
+  uint8_t* smem;          // dynamic shared memory base
+  const uint64_t* decode; // [256]
+  const uint8_t* gray;    // GRAY84: gray LUT in smem; RAW: nullptr
+  uint32_t rom0;          // smem offset of the ROM images
+  uint32_t ram0;          // smem offset of this thread's RAM word 0 (stride ram_stride)
+  uint32_t ram_stride;    // bytes between RAM words of one thread (4 * blockDim)
+  uint32_t* tw;           // this thread's TIA words        (stride s)
+  uint32_t* pw;           // this thread's pixel-writer words
+  uint32_t* lg;           // this thread's TIA write log
+  uint32_t s;             // word stride = blockDim
+  uint32_t ystart, line_cap;
+};
 
-// Run until the frame ends (VSYNC rise), a fault, or max_instr instructions (<0: unlimited).
-template <bool kGray>
-__device__ int32_t run_frame(Machine& m, uint32_t line_cap, int32_t max_instr) {
-  int32_t count = 0;
-  for (;;) {
-    if (max_instr >= 0 && count >= max_instr) {
-      m.catch_up<kGray>(3u * m.fc);
-      m.t_phaseA = m.t_tia;
-      return RUN_BUDGET;
+struct Cpu {
+  uint32_t PC, A, X, Y, SP, C, V, D, I, nreg, zreg;
+  uint32_t fc, now, t_phaseA;
+  uint32_t bank, rom_off, is_f8, flim;
+  uint32_t tV, tS, swcha, inpt4;
+  int32_t tW;
+  uint32_t vsync, log_len, fault;
+
+  __device__ __forceinline__ uint32_t getP() const {
+    return (nreg & 0x80u) | (V << 6) | 0x20u | (D << 3) | (I << 2) | ((zreg & 0xFFu) == 0 ? 2u : 0u) | C;
+  }
+  __device__ __forceinline__ void setP(uint32_t p) {
+    nreg = p & 0x80u; V = (p >> 6) & 1u; D = (p >> 3) & 1u; I = (p >> 2) & 1u;
+    zreg = (p & 2u) ? 0u : 1u; C = p & 1u;
+  }
+
+  __device__ __forceinline__ uint32_t ram_addr(const Ctx& c, uint32_t a) const {
+    return c.ram0 + (a >> 2) * c.ram_stride + (a & 3u);
+  }
+  __device__ __forceinline__ uint32_t ram_rd(const Ctx& c, uint32_t a) const { return c.smem[ram_addr(c, a & 0x7Fu)]; }
+
+  // RIOT interval timer, closed form from the write stamp (DESIGN.md §2 R#24)
+  __device__ __forceinline__ uint32_t riot_read(uint32_t a) const {
+    if (!(a & 0x04u)) {
+      uint32_t k = a & 3u;
+      return k == 0 ? swcha : (k == 2 ? 0x0Bu : 0u);
     }
-    bool jam = false;
-    uint32_t n = exec_one<kGray>(m, jam);
-    if (jam) {
-      m.catch_up<kGray>(3u * m.fc);
-      return RUN_JAM;
+    int32_t e = (int32_t)now - tW;
+    int32_t VI = (int32_t)(tV << tS);
+    if (a & 1u) return e > VI ? 0x80u : 0u;
+    if (e <= VI) return (tV - (uint32_t)((e + (1 << tS) - 1) >> tS)) & 0xFFu;
+    return (uint32_t)(0xFF - (e - VI - 1)) & 0xFFu;
+  }
+
+  // collision-latch read: flush this lane's log (divergent but rare) and advance to t
+  __device__ __forceinline__ uint32_t tia_coll_read(const Ctx& c, uint32_t r, uint32_t t) {
+    const uint32_t coll = coll_read_flush(c.tw, c.pw, c.lg, c.s, log_len, t, c.ystart, c.gray);
+    log_len = 0;
+    return (((coll >> (2 * r)) & 1u) << 7) | (((coll >> (2 * r + 1)) & 1u) << 6);
+  }
+
+  // full bus read; phase A (fetch / pointer) or phase C (data) — DESIGN.md §2 R#4
+  template <bool kPhaseA>
+  __device__ __forceinline__ uint32_t rd(const Ctx& c, uint32_t addr) {
+    const uint32_t a = addr & 0x1FFFu;
+    const bool cart = (a & 0x1000u) != 0;
+    const bool hot = cart && is_f8 && ((a & 0x1FFEu) == 0x1FF8u);
+    const bool ram = !cart && ((a & 0x0280u) == 0x0080u);
+    if (cart | ram) {
+      if (hot) bank = a & 1u;
+      const uint32_t off = cart ? c.rom0 + rom_off + (bank << 12) + (a & 0xFFFu) : ram_addr(c, a & 0x7Fu);
+      return c.smem[off];
     }
-    ++count;
-    m.fc += n;
-    m.t_phaseA = 3u * m.fc;
-    if (m.wsync_req) m.fc = ((m.fc + 75u) / 76u) * 76u;
-    if (m.fc / 76u >= line_cap) {
-      m.catch_up<kGray>(3u * m.fc);
-      return RUN_RUNAWAY;
+    if (!(a & 0x80u)) {  // TIA read registers
+      const uint32_t r = a & 0x0Fu;
+      if (r < 8u) return tia_coll_read(c, r, kPhaseA ? t_phaseA : 3u * now);
+      return r == 0x0Cu ? inpt4 : (r == 0x0Du ? 0x80u : 0u);
     }
-    if (m.vsync_rose) {
-      end_frame<kGray>(m);
-      return RUN_FRAME;
+    return riot_read(a);
+  }
+
+  __device__ __forceinline__ void wr(const Ctx& c, uint32_t addr, uint32_t v) {
+    const uint32_t a = addr & 0x1FFFu;
+    if ((a & 0x1280u) == 0x0080u) { c.smem[ram_addr(c, a & 0x7Fu)] = (uint8_t)v; return; }
+    if (a & 0x1000u) {
+      if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+      return;
+    }
+    if (!(a & 0x80u)) {
+      const uint32_t r = a & 0x3Fu;
+      if (r == 0x02u) { wsync_pending = 1; return; }
+      if (r == 0x00u) {
+        uint32_t nv = (v >> 1) & 1u;
+        if (!vsync && nv) vsync_rose = 1;
+        vsync = nv;
+        return;
+      }
+      if (r == 0x03u || (r >= 0x15u && r <= 0x1Au) || r >= 0x2Du) return;  // no TIA effect
+      c.lg[log_len * c.s] = log_entry(3u * now, r, v);
+      ++log_len;
+      return;
+    }
+    if ((a & 0x14u) == 0x14u) {  // timer write: interval 1 / 8 / 64 / 1024
+      tV = v & 0xFFu;
+      tS = (0xA630u >> (4 * (a & 3u))) & 0xFu;
+      tW = (int32_t)now;
     }
   }
-}
+  uint32_t wsync_pending, vsync_rose;
+
+  __device__ __forceinline__ void push(const Ctx& c, uint32_t v) { wr(c, 0x100u | SP, v); SP = (SP - 1) & 0xFFu; }
+  __device__ __forceinline__ uint32_t pull(const Ctx& c) { SP = (SP + 1) & 0xFFu; return rd<false>(c, 0x100u | SP); }
+
+  // ---- one instruction; returns an Event ------------------------------------------------------
+  __device__ __forceinline__ uint32_t exec(const Ctx& c) {
+    now = fc;
+    wsync_pending = 0;
+    vsync_rose = 0;
+    const uint32_t pc = PC;
+    uint32_t op, b1, b2;
+    uint64_t d;
+    if ((pc & 0x1000u) && (pc & 0xFFFu) <= flim) {
+      const uint8_t* p = c.smem + c.rom0 + rom_off + (bank << 12) + (pc & 0xFFFu);
+      op = p[0]; b1 = p[1]; b2 = p[2];
+      d = c.decode[op];
+    } else {
+      op = rd<true>(c, pc);
+      d = c.decode[op];
+      const uint32_t len = (uint32_t)(d >> dk::LEN) & 3u;
+      b1 = len > 1 ? rd<true>(c, pc + 1) : 0u;
+      b2 = len > 2 ? rd<true>(c, pc + 2) : 0u;
+    }
+    const uint32_t lo32 = (uint32_t)d, hi32 = (uint32_t)(d >> 32);
+    const uint32_t spc = (hi32 >> (dk::SPC - 32)) & 0xFu;
+    if (spc == SP_JAM) { PC = (pc + 1) & 0xFFFFu; fault = 1; return EV_FAULT; }
+    const uint32_t mode = lo32 & 0xFu;
+    uint32_t n = (lo32 >> dk::CYC) & 0xFu;
+    PC = (pc + ((lo32 >> dk::LEN) & 3u)) & 0xFFFFu;
+
+    // ---- phase A: effective address (all modes computed arithmetically) ----------------------
+    const uint32_t zidx = (mode == AM_ZPX || mode == AM_INDX) ? X : (mode == AM_ZPY ? Y : 0u);
+    const uint32_t zpa = (b1 + zidx) & 0xFFu;
+    uint32_t base = b1 | (b2 << 8);
+    if (mode == AM_INDX || mode == AM_INDY || mode == AM_IND) {
+      const uint32_t p0 = mode == AM_IND ? base : zpa;
+      const uint32_t p1 = mode == AM_IND ? ((base & 0xFF00u) | ((base + 1) & 0xFFu)) : ((zpa + 1) & 0xFFu);
+      const uint32_t plo = rd<true>(c, p0);
+      const uint32_t phi = rd<true>(c, p1);
+      base = plo | (phi << 8);
+    }
+    const uint32_t aidx = mode == AM_ABSX ? X : ((mode == AM_ABSY || mode == AM_INDY) ? Y : 0u);
+    const uint32_t ea16 = (base + aidx) & 0xFFFFu;
+    const bool zpmode = mode == AM_ZP || mode == AM_ZPX || mode == AM_ZPY;
+    const uint32_t ea = zpmode ? zpa : ea16;
+    n += ((lo32 >> dk::PEN) & 1u) & (((ea16 ^ base) >> 8) & 1u);
+    if ((hi32 >> (dk::BR - 32)) & 1u) {
+      const uint32_t sel = (hi32 >> (dk::BRF - 32)) & 3u;
+      const uint32_t flag = sel == 0 ? (nreg >> 7) & 1u : sel == 1 ? V : sel == 2 ? C : ((zreg & 0xFFu) == 0 ? 1u : 0u);
+      if (flag == ((hi32 >> (dk::BRT - 32)) & 1u)) {
+        const uint32_t tgt = (PC + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
+        n += 1u + (((tgt ^ PC) >> 8) & 1u);
+        PC = tgt;
+      }
+    }
+    if ((hi32 >> (dk::JMP - 32)) & 1u) PC = ea;
+
+    // ---- phase C ------------------------------------------------------------------------------
+    now = fc + n;
+    uint32_t v = b1;  // immediate operand
+    if ((lo32 >> dk::RD) & 1u) v = rd<false>(c, ea);
+
+    if (spc) {
+      special(c, spc, v, ea);
+    } else {
+      const uint32_t rsrc = (lo32 >> dk::RSRC) & 3u;
+      const uint32_t R = rsrc == RG_A ? A : rsrc == RG_X ? X : rsrc == RG_Y ? Y : SP;
+      const uint32_t M = ((lo32 >> dk::OPR) & 1u) ? R : v;
+      const uint32_t u1 = (lo32 >> dk::U1) & 7u, u2 = (lo32 >> dk::U2) & 7u;
+      // unit1: shifts / rotates / inc / dec
+      const bool sl = u1 == U1_ASL || u1 == U1_ROL, sr = u1 == U1_LSR || u1 == U1_ROR;
+      const uint32_t shl = ((M << 1) | (u1 == U1_ROL ? C : 0u)) & 0xFFu;
+      const uint32_t shr = (M >> 1) | (u1 == U1_ROR ? (C << 7) : 0u);
+      const uint32_t idc = (M + (u1 == U1_INC ? 1u : (u1 == U1_DEC ? 0xFFu : 0u))) & 0xFFu;
+      const uint32_t r1 = sl ? shl : (sr ? shr : idc);
+      const uint32_t c1 = sl ? (M >> 7) : (sr ? (M & 1u) : C);
+      // unit2: logic / adder (ADC, SBC, CMP share it) / BIT
+      const bool cmp = u2 == U2_CMP, sub = u2 == U2_SBC || cmp, arith = u2 >= U2_ADC && u2 <= U2_CMP;
+      const uint32_t lhs = cmp ? R : A;
+      const uint32_t add = sub ? (r1 ^ 0xFFu) : r1;
+      const uint32_t sum = lhs + add + (cmp ? 1u : c1);
+      const uint32_t rlog = u2 == U2_OR ? (A | r1) : (u2 == U2_AND ? (A & r1) : (A ^ r1));
+      uint32_t r2 = u2 == U2_PASS ? r1 : (arith ? (sum & 0xFFu) : rlog);
+      uint32_t nC = arith ? (sum >> 8) : c1;
+      uint32_t nV = (u2 == U2_ADC || u2 == U2_SBC) ? ((~(lhs ^ add) & (lhs ^ sum)) >> 7) & 1u
+                  : (u2 == U2_BIT ? (r1 >> 6) & 1u : V);
+      uint32_t nn = u2 == U2_BIT ? r1 : r2, nz_ = u2 == U2_BIT ? (A & r1) : r2;
+      if (D && (u2 == U2_ADC || u2 == U2_SBC)) decimal(u2, r1, c1, r2, nC, nV, nn, nz_);
+      if ((lo32 >> dk::WR) & 1u) {
+        const uint32_t sv = ((lo32 >> dk::SAX) & 1u) ? (A & X) : R;
+        wr(c, ea, ((lo32 >> dk::WSEL) & 1u) ? sv : r1);
+      }
+      const uint32_t dst = (lo32 >> dk::DST) & 7u;
+      if (dst == DS_A || dst == DS_AX) A = r2;
+      if (dst == DS_X || dst == DS_AX) X = r2;
+      if (dst == DS_Y) Y = r2;
+      if (dst == DS_SP) SP = r2;
+      if ((lo32 >> dk::NZ) & 1u) { nreg = nn; zreg = nz_ & 0xFFu; }
+      C = nC;
+      V = nV;
+      if ((lo32 >> dk::FOP) & 1u) {
+        const uint32_t fi = (lo32 >> dk::FIDX) & 3u, fv = (lo32 >> dk::FVAL) & 1u;
+        if (fi == 0) C = fv;
+        if (fi == 1) I = fv;
+        if (fi == 2) D = fv;
+        if (fi == 3) V = fv;
+      }
+    }
+
+    // ---- end of instruction ----------------------------------------------------------------------
+    fc = now;
+    t_phaseA = 3u * now;
+    if (wsync_pending) fc = ((fc + 75u) / 76u) * 76u;  // stall to the next line start (R#5)
+    if (fc / 76u >= c.line_cap) { fault = 2; return EV_FAULT; }
+    if (vsync_rose) return EV_FRAME;
+    return log_len > (uint32_t)(kLogCap - kLogMargin) ? EV_LOGFULL : EV_NONE;
+  }
+
+  // NMOS decimal ADC / SBC (Bruce Clark's sequences, DESIGN.md §2 R#2)
+  __device__ __forceinline__ void decimal(uint32_t u2, uint32_t m, uint32_t cin, uint32_t& r2, uint32_t& nC,
+                                       uint32_t& nV, uint32_t& nn, uint32_t& nz_) const {
+    if (u2 == U2_ADC) {
+      uint32_t lo = (A & 0xFu) + (m & 0xFu) + cin;
+      if (lo >= 0xAu) lo = ((lo + 6u) & 0xFu) + 0x10u;
+      uint32_t s = (A & 0xF0u) + (m & 0xF0u) + lo;
+      int32_t sv = (int32_t)(int8_t)(A & 0xF0u) + (int32_t)(int8_t)(m & 0xF0u) + (int32_t)lo;
+      nz_ = (A + m + cin) & 0xFFu;
+      nn = s;
+      nV = (sv < -128 || sv > 127) ? 1u : 0u;
+      if (s >= 0xA0u) s += 0x60u;
+      nC = s >= 0x100u ? 1u : 0u;
+      r2 = s & 0xFFu;
+    } else {
+      int32_t lo = (int32_t)(A & 0xFu) - (int32_t)(m & 0xFu) + (int32_t)cin - 1;
+      if (lo < 0) lo = ((lo - 6) & 0xF) - 0x10;
+      int32_t s = (int32_t)(A & 0xF0u) - (int32_t)(m & 0xF0u) + lo;
+      if (s < 0) s -= 0x60;
+      r2 = (uint32_t)s & 0xFFu;  // flags stay binary
+    }
+  }
+
+  // stack / control flow / immediate undocumented ops
+  __device__ __forceinline__ void special(const Ctx& c, uint32_t spc, uint32_t v, uint32_t ea) {
+    switch (spc) {
+      case SP_PHA: push(c, A); break;
+      case SP_PHP: push(c, getP() | 0x30u); break;
+      case SP_PLA: A = pull(c); nreg = A; zreg = A; break;
+      case SP_PLP: setP(pull(c)); break;
+      case SP_JSR: {
+        const uint32_t ret = (PC - 1) & 0xFFFFu;
+        push(c, ret >> 8);
+        push(c, ret & 0xFFu);
+        PC = ea;
+      } break;
+      case SP_RTS: {
+        const uint32_t lo = pull(c);
+        const uint32_t hi = pull(c);
+        PC = ((lo | (hi << 8)) + 1) & 0xFFFFu;
+      } break;
+      case SP_RTI: {
+        setP(pull(c));
+        const uint32_t lo = pull(c);
+        const uint32_t hi = pull(c);
+        PC = lo | (hi << 8);
+      } break;
+      case SP_BRK: {
+        const uint32_t ret = (PC + 1) & 0xFFFFu;
+        push(c, ret >> 8);
+        push(c, ret & 0xFFu);
+        push(c, getP() | 0x30u);
+        I = 1;
+        const uint32_t lo = rd<false>(c, 0x1FFEu);
+        const uint32_t hi = rd<false>(c, 0x1FFFu);
+        PC = lo | (hi << 8);
+      } break;
+      case SP_ANC: A &= v; nreg = A; zreg = A; C = A >> 7; break;
+      case SP_ALR: { uint32_t t = A & v; C = t & 1u; A = t >> 1; nreg = A; zreg = A; } break;
+      case SP_ARR: {
+        uint32_t t = A & v;
+        A = (t >> 1) | (C << 7);
+        nreg = A; zreg = A;
+        C = (A >> 6) & 1u;
+        V = ((A >> 6) ^ (A >> 5)) & 1u;
+      } break;
+      case SP_SBX: { uint32_t t = A & X; C = t >= v ? 1u : 0u; X = (t - v) & 0xFFu; nreg = X; zreg = X; } break;
+      default: break;
+    }
+  }
+};
 
 }  // namespace cule

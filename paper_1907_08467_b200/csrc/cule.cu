@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -50,7 +51,7 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   L->cscore = take(2 * nk);
   L->cstage = take(gray ? nk * cule::kFrameBytes : 0);
   L->roms = take(4 * 8192);
-  L->decode = take(1024);
+  L->decode = take(2048);
   L->gray = take(128);
   L->counters = take(32);
   L->err = take(16);
@@ -74,6 +75,7 @@ struct cule_env {
   uint32_t f8_mask;
   uint64_t pick_seed;
   size_t smem;
+  uint32_t block;
 };
 
 static cule::Params base_params(const cule_env* e) {
@@ -87,7 +89,7 @@ static cule::Params base_params(const cule_env* e) {
   for (int r = 0; r < 4; ++r) p.rom_off[r] = e->rom_off[r];
   p.f8_mask = e->f8_mask;
   p.n_roms = (uint32_t)e->n_roms;
-  p.decode = reinterpret_cast<const uint32_t*>(e->ws + e->L.decode);
+  p.decode = reinterpret_cast<const uint64_t*>(e->ws + e->L.decode);
   p.gray = e->ws + e->L.gray;
   p.cache_state = e->ws + e->L.cstate;
   p.cache_score = reinterpret_cast<const uint16_t*>(e->ws + e->L.cscore);
@@ -127,7 +129,22 @@ static int cuda_check(const char* what) {
   return CULE_OK;
 }
 
-static constexpr int kBlock = 128;
+static constexpr int kMaxBlock = 128;
+
+// threads per block: small blocks spread few envs over all SMs (the low-env regime is
+// latency-bound); CULE_BLOCK overrides (32, 64 or 128)
+static uint32_t choose_block(int N) {
+  if (const char* v = getenv("CULE_BLOCK")) {
+    int b = atoi(v);
+    if (b == 32 || b == 64 || b == 128) return (uint32_t)b;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint32_t b = 128;
+  while (b > 32 && ((uint32_t)N + b - 1) / b < 2u * (uint32_t)sms) b /= 2;
+  return b;
+}
 
 extern "C" {
 
@@ -170,6 +187,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
       cfg->line_cap < 1 || cfg->ystart < 0 || cfg->ystart + cule::kFrameH > cfg->line_cap ||
       cfg->max_episode_frames < 0)
     return fail(CULE_E_INVAL, "bad config value");
+  if (cfg->line_cap > 1024) return fail(CULE_E_INVAL, "line_cap must be <= 1024 (18-bit log timestamps)");
   if (cfg->score_addr < 0x80 || cfg->score_addr == 0xFF || cfg->term_addr < 0x80)
     return fail(CULE_E_INVAL, "score/terminal addresses must be RAM bus addresses $80-$FF");
   if (cfg->obs_mode == CULE_OBS_GRAY84 && !cfg->palette_rgb)
@@ -204,12 +222,14 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     if (rom_lens[r] == 8192) e->f8_mask |= 1u << r;
   }
   e->rom_bytes = off;
-  e->smem = cule::smem_bytes(e->rom_bytes, kBlock);
+  e->block = choose_block(num_envs);
+  e->smem = cule::smem_bytes(e->rom_bytes, e->block);
+  const size_t smem_max = cule::smem_bytes(e->rom_bytes, kMaxBlock);
 
   // static inputs: ROM images, decode table, gray LUT (ITU-R 601 integer, half-up, §8(c).12)
   uint8_t romimg[4 * 8192];
   for (int r = 0; r < n_roms; ++r) std::memcpy(romimg + e->rom_off[r], roms[r], rom_lens[r]);
-  uint32_t table[256];
+  uint64_t table[256];
   cule::build_decode_table(table);
   uint8_t gray[128] = {0};
   if (cfg->palette_rgb) {
@@ -228,18 +248,20 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   if (rc) { delete e; return rc; }
 
   const bool g = cfg->obs_mode == CULE_OBS_GRAY84;
-  cudaFuncSetAttribute(cule::step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  cudaFuncSetAttribute(cule::step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  cudaFuncSetAttribute(cule::cache_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  cudaFuncSetAttribute(cule::cache_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
-  cudaFuncSetAttribute(cule::debug_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->smem);
+  cudaFuncSetAttribute(cule::step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(cule::step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(cule::cache_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(cule::cache_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(cule::debug_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
 
   // reset cache build: one thread per (rom, entry)
   cule::Params p = base_params(e);
   const uint32_t total = (uint32_t)n_roms * (uint32_t)cfg->reset_cache_size;
-  const uint32_t blocks = (total + kBlock - 1) / kBlock;
-  if (g) cule::cache_kernel<true><<<blocks, kBlock, e->smem>>>(p);
-  else cule::cache_kernel<false><<<blocks, kBlock, e->smem>>>(p);
+  const uint32_t cblock = 32;
+  const size_t csmem = cule::smem_bytes(e->rom_bytes, cblock);
+  const uint32_t blocks = (total + cblock - 1) / cblock;
+  if (g) cule::cache_kernel<true><<<blocks, cblock, csmem>>>(p);
+  else cule::cache_kernel<false><<<blocks, cblock, csmem>>>(p);
   rc = cuda_check("cache_kernel launch");
   if (rc) { delete e; return rc; }
   int32_t err_flag = 0;
@@ -279,9 +301,9 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
   p.obs = static_cast<uint8_t*>(d_obs);
   p.rewards = d_rewards;
   p.dones = d_dones;
-  const uint32_t blocks = ((uint32_t)e->N + kBlock - 1) / kBlock;
-  if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::step_kernel<true><<<blocks, kBlock, e->smem, s>>>(p);
-  else cule::step_kernel<false><<<blocks, kBlock, e->smem, s>>>(p);
+  const uint32_t blocks = ((uint32_t)e->N + e->block - 1) / e->block;
+  if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::step_kernel<true><<<blocks, e->block, e->smem, s>>>(p);
+  else cule::step_kernel<false><<<blocks, e->block, e->smem, s>>>(p);
   return cuda_check("step_kernel");
 }
 
@@ -348,8 +370,8 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
   cule::Params p = base_params(e);
   p.debug_instr = n_instr;
   p.debug_status = d_status;
-  const uint32_t blocks = ((uint32_t)e->N + kBlock - 1) / kBlock;
-  cule::debug_kernel<<<blocks, kBlock, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
+  const uint32_t blocks = ((uint32_t)e->N + e->block - 1) / e->block;
+  cule::debug_kernel<<<blocks, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
   return cuda_check("debug_kernel");
 }
 

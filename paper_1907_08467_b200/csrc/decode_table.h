@@ -1,16 +1,17 @@
-// decode_table.h — host-side construction of the 6502 decode/cycle table used by the step
-// kernel (staged into shared memory once per block).  Product code; independent of the oracle.
+// decode_table.h — host-side construction of the 6502 micro-coded decode table used by the
+// step kernel (one 64-bit entry per opcode, staged into shared memory once per block).
+// Product code; independent of the oracle (which executes a per-opcode switch).
 //
-// Entry layout (u32):
-//   bits 0-3   addressing mode (AM_*)
-//   bits 4-10  operation (OP_*)
-//   bits 11-14 base cycle count
-//   bit  15    +1 cycle when the effective address crosses a page (read-class abs,X/abs,Y/(zp),Y)
-//   bit  16    the operation reads its operand from memory (phase-C data read)
-//   bits 17-18 branch flag selector (0 N, 1 V, 2 C, 3 Z), bit 19 = branch taken when flag set
+// The kernel runs every ordinary instruction through ONE branch-free datapath:
+//   R  = register operand (A/X/Y/SP);  M = memory/immediate byte, or R for implied forms
+//   u1 = unit1(M): pass | ASL | LSR | ROL | ROR | INC | DEC   (carry c1)
+//   r2 = unit2(u1): pass | OR | AND | EOR | ADC | SBC | CMP(R) | BIT  (8-bit adder shared)
+//   then destination register, memory write value, N/Z/C/V updates — all selected by fields
+// so lanes executing different opcodes still share instructions.  Stack/control and the
+// rare undocumented immediates take a small "special" switch.
 //
-// Cycle counts are derived from the addressing-mode / access-class rules of the NMOS 6502
-// (bottom table), not copied per opcode.
+// Cycle counts derive from the addressing-mode x access-class rules of the NMOS 6502
+// (bottom table), not from a per-opcode list.
 #pragma once
 #include <stdint.h>
 
@@ -23,25 +24,50 @@ enum AddrMode : uint32_t {
   AM_IMP = 0, AM_ACC, AM_IMM, AM_ZP, AM_ZPX, AM_ZPY, AM_ABS, AM_ABSX, AM_ABSY, AM_IND,
   AM_INDX, AM_INDY, AM_REL
 };
-
-enum Op : uint32_t {
-  OP_JAM = 0,
-  OP_LDA, OP_LDX, OP_LDY, OP_LAX,
-  OP_STA, OP_STX, OP_STY, OP_SAX,
-  OP_ORA, OP_AND, OP_EOR, OP_ADC, OP_SBC, OP_CMP, OP_CPX, OP_CPY, OP_BIT,
-  OP_ASL, OP_LSR, OP_ROL, OP_ROR, OP_INC, OP_DEC,
-  OP_SLO, OP_RLA, OP_SRE, OP_RRA, OP_DCP, OP_ISB,
-  OP_ANC, OP_ALR, OP_ARR, OP_SBX,
-  OP_NOP,
-  OP_INX, OP_INY, OP_DEX, OP_DEY, OP_TAX, OP_TAY, OP_TXA, OP_TYA, OP_TSX, OP_TXS,
-  OP_CLC, OP_SEC, OP_CLI, OP_SEI, OP_CLV, OP_CLD, OP_SED,
-  OP_PHA, OP_PHP, OP_PLA, OP_PLP,
-  OP_JMP, OP_JSR, OP_RTS, OP_RTI, OP_BRK,
-  OP_BRANCH,
-  OP_COUNT
+enum Unit1 : uint32_t { U1_PASS = 0, U1_ASL, U1_LSR, U1_ROL, U1_ROR, U1_INC, U1_DEC };
+enum Unit2 : uint32_t { U2_PASS = 0, U2_OR, U2_AND, U2_EOR, U2_ADC, U2_SBC, U2_CMP, U2_BIT };
+enum Reg : uint32_t { RG_A = 0, RG_X, RG_Y, RG_SP };
+enum Dst : uint32_t { DS_NONE = 0, DS_A, DS_X, DS_Y, DS_SP, DS_AX };
+enum Special : uint32_t {
+  SP_NONE = 0, SP_PHA, SP_PHP, SP_PLA, SP_PLP, SP_JSR, SP_RTS, SP_RTI, SP_BRK, SP_ANC, SP_ALR,
+  SP_ARR, SP_SBX, SP_JAM
 };
 
-enum AccessClass { CL_READ, CL_WRITE, CL_RMW, CL_FIXED };
+// bit fields of an entry
+namespace dk {
+constexpr int MODE = 0;     // 4 bits
+constexpr int LEN = 4;      // 2 bits: instruction length 1..3
+constexpr int CYC = 6;      // 4 bits: base cycles
+constexpr int PEN = 10;     // 1: +1 on page cross
+constexpr int RD = 11;      // 1: data read at EA
+constexpr int WR = 12;      // 1: data write at EA
+constexpr int RSRC = 13;    // 2: register operand R
+constexpr int OPR = 15;     // 1: M = R (implied/accumulator forms)
+constexpr int U1 = 16;      // 3
+constexpr int U2 = 19;      // 3
+constexpr int DST = 22;     // 3
+constexpr int WSEL = 25;    // 1: write value = store value (R, or A&X) instead of u1
+constexpr int SAX = 26;     // 1: store value A&X
+constexpr int NZ = 27;      // 1: update N/Z
+constexpr int FOP = 28;     // 1: flag set/clear op
+constexpr int FIDX = 29;    // 2: 0 C, 1 I, 2 D, 3 V
+constexpr int FVAL = 31;    // 1
+constexpr int SPC = 32;     // 4: special op
+constexpr int BR = 36;      // 1: conditional branch
+constexpr int BRF = 37;     // 2: branch flag 0 N 1 V 2 C 3 Z
+constexpr int BRT = 39;     // 1: taken when flag set
+constexpr int JMP = 40;     // 1: PC <- EA
+}  // namespace dk
+
+inline uint32_t mode_len(uint32_t mode) {
+  switch (mode) {
+    case AM_IMP: case AM_ACC: return 1;
+    case AM_ABS: case AM_ABSX: case AM_ABSY: case AM_IND: return 3;
+    default: return 2;
+  }
+}
+
+enum AccessClass { CL_READ, CL_WRITE, CL_RMW };
 
 inline uint32_t mode_cycles(uint32_t mode, AccessClass cl, bool* pen) {
   *pen = false;
@@ -61,91 +87,154 @@ inline uint32_t mode_cycles(uint32_t mode, AccessClass cl, bool* pen) {
   }
 }
 
-struct OpModes { uint32_t op; AccessClass cl; struct { uint32_t mode; uint8_t opc; } m[8]; int n; };
+struct Micro {
+  uint32_t u1 = U1_PASS, u2 = U2_PASS, rsrc = RG_A, dst = DS_NONE;
+  bool opr = false, wsel = false, sax = false, nz = false;
+};
 
-inline void build_decode_table(uint32_t* table) {
-  for (int i = 0; i < 256; i++) table[i] = OP_JAM << 4; /* JAM and unstable opcodes fault */
-  auto put = [&](uint32_t opc, uint32_t mode, uint32_t op, uint32_t cyc, bool pen, bool rd) {
-    table[opc] = mode | (op << 4) | (cyc << 11) | ((pen ? 1u : 0u) << 15) | ((rd ? 1u : 0u) << 16);
-  };
-  auto group = [&](uint32_t op, AccessClass cl, std::initializer_list<std::pair<uint32_t, uint32_t>> ms) {
+inline uint64_t entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr, const Micro& u) {
+  uint64_t e = 0;
+  e |= (uint64_t)mode << dk::MODE;
+  e |= (uint64_t)mode_len(mode) << dk::LEN;
+  e |= (uint64_t)cyc << dk::CYC;
+  e |= (uint64_t)(pen ? 1 : 0) << dk::PEN;
+  e |= (uint64_t)(rd ? 1 : 0) << dk::RD;
+  e |= (uint64_t)(wr ? 1 : 0) << dk::WR;
+  e |= (uint64_t)u.rsrc << dk::RSRC;
+  e |= (uint64_t)(u.opr ? 1 : 0) << dk::OPR;
+  e |= (uint64_t)u.u1 << dk::U1;
+  e |= (uint64_t)u.u2 << dk::U2;
+  e |= (uint64_t)u.dst << dk::DST;
+  e |= (uint64_t)(u.wsel ? 1 : 0) << dk::WSEL;
+  e |= (uint64_t)(u.sax ? 1 : 0) << dk::SAX;
+  e |= (uint64_t)(u.nz ? 1 : 0) << dk::NZ;
+  return e;
+}
+
+inline void build_decode_table(uint64_t* table) {
+  for (int i = 0; i < 256; i++) table[i] = ((uint64_t)SP_JAM << dk::SPC) | (1ull << dk::LEN);
+  auto group = [&](const Micro& u, AccessClass cl, std::initializer_list<std::pair<uint32_t, uint32_t>> ms) {
     for (auto& p : ms) {
       bool pen;
       uint32_t cyc = mode_cycles(p.first, cl, &pen);
       bool rd = (cl == CL_READ && p.first != AM_IMM) || cl == CL_RMW;
-      put(p.second, p.first, op, cyc, pen, rd);
+      bool wr = cl != CL_READ;
+      table[p.second] = entry(p.first, cyc, pen, rd, wr, u);
     }
   };
-  // the eight-mode ALU group (ORA AND EOR ADC LDA CMP SBC): aaa bbb 01
-  const uint32_t alu8[7][2] = {{OP_ORA, 0x00}, {OP_AND, 0x20}, {OP_EOR, 0x40}, {OP_ADC, 0x60},
-                               {OP_LDA, 0xA0}, {OP_CMP, 0xC0}, {OP_SBC, 0xE0}};
+  auto mk = [](uint32_t u1, uint32_t u2, uint32_t rsrc, uint32_t dst, bool nz) {
+    Micro m;
+    m.u1 = u1; m.u2 = u2; m.rsrc = rsrc; m.dst = dst; m.nz = nz;
+    return m;
+  };
+  // eight-mode ALU group aaa bbb 01
+  const uint32_t alu8[7][3] = {{U2_OR, 0x00, DS_A}, {U2_AND, 0x20, DS_A}, {U2_EOR, 0x40, DS_A},
+                               {U2_ADC, 0x60, DS_A}, {U2_PASS, 0xA0, DS_A}, {U2_CMP, 0xC0, DS_NONE},
+                               {U2_SBC, 0xE0, DS_A}};
   for (auto& g : alu8) {
     uint32_t b = g[1];
-    group(g[0], CL_READ, {{AM_INDX, b + 0x01}, {AM_ZP, b + 0x05}, {AM_IMM, b + 0x09},
-                          {AM_ABS, b + 0x0D}, {AM_INDY, b + 0x11}, {AM_ZPX, b + 0x15},
-                          {AM_ABSY, b + 0x19}, {AM_ABSX, b + 0x1D}});
+    group(mk(U1_PASS, g[0], RG_A, g[2], true), CL_READ,
+          {{AM_INDX, b + 0x01}, {AM_ZP, b + 0x05}, {AM_IMM, b + 0x09}, {AM_ABS, b + 0x0D},
+           {AM_INDY, b + 0x11}, {AM_ZPX, b + 0x15}, {AM_ABSY, b + 0x19}, {AM_ABSX, b + 0x1D}});
   }
-  group(OP_STA, CL_WRITE, {{AM_INDX, 0x81}, {AM_ZP, 0x85}, {AM_ABS, 0x8D}, {AM_INDY, 0x91},
-                           {AM_ZPX, 0x95}, {AM_ABSY, 0x99}, {AM_ABSX, 0x9D}});
-  group(OP_LDX, CL_READ, {{AM_IMM, 0xA2}, {AM_ZP, 0xA6}, {AM_ABS, 0xAE}, {AM_ZPY, 0xB6}, {AM_ABSY, 0xBE}});
-  group(OP_LDY, CL_READ, {{AM_IMM, 0xA0}, {AM_ZP, 0xA4}, {AM_ABS, 0xAC}, {AM_ZPX, 0xB4}, {AM_ABSX, 0xBC}});
-  group(OP_STX, CL_WRITE, {{AM_ZP, 0x86}, {AM_ABS, 0x8E}, {AM_ZPY, 0x96}});
-  group(OP_STY, CL_WRITE, {{AM_ZP, 0x84}, {AM_ABS, 0x8C}, {AM_ZPX, 0x94}});
-  group(OP_CPX, CL_READ, {{AM_IMM, 0xE0}, {AM_ZP, 0xE4}, {AM_ABS, 0xEC}});
-  group(OP_CPY, CL_READ, {{AM_IMM, 0xC0}, {AM_ZP, 0xC4}, {AM_ABS, 0xCC}});
-  group(OP_BIT, CL_READ, {{AM_ZP, 0x24}, {AM_ABS, 0x2C}});
-  // shifts/rotates/inc/dec: aaa bbb 10
-  const uint32_t rmw[6][2] = {{OP_ASL, 0x00}, {OP_ROL, 0x20}, {OP_LSR, 0x40}, {OP_ROR, 0x60},
-                              {OP_DEC, 0xC0}, {OP_INC, 0xE0}};
+  group(mk(U1_PASS, U2_SBC, RG_A, DS_A, true), CL_READ, {{AM_IMM, 0xEB}});
+  auto store = [&](uint32_t rsrc, bool sax) {
+    Micro m;
+    m.rsrc = rsrc; m.wsel = true; m.sax = sax;
+    return m;
+  };
+  group(store(RG_A, false), CL_WRITE, {{AM_INDX, 0x81}, {AM_ZP, 0x85}, {AM_ABS, 0x8D}, {AM_INDY, 0x91},
+                                       {AM_ZPX, 0x95}, {AM_ABSY, 0x99}, {AM_ABSX, 0x9D}});
+  group(store(RG_X, false), CL_WRITE, {{AM_ZP, 0x86}, {AM_ABS, 0x8E}, {AM_ZPY, 0x96}});
+  group(store(RG_Y, false), CL_WRITE, {{AM_ZP, 0x84}, {AM_ABS, 0x8C}, {AM_ZPX, 0x94}});
+  group(store(RG_A, true), CL_WRITE, {{AM_INDX, 0x83}, {AM_ZP, 0x87}, {AM_ABS, 0x8F}, {AM_ZPY, 0x97}});
+  group(mk(U1_PASS, U2_PASS, RG_A, DS_X, true), CL_READ,
+        {{AM_IMM, 0xA2}, {AM_ZP, 0xA6}, {AM_ABS, 0xAE}, {AM_ZPY, 0xB6}, {AM_ABSY, 0xBE}});
+  group(mk(U1_PASS, U2_PASS, RG_A, DS_Y, true), CL_READ,
+        {{AM_IMM, 0xA0}, {AM_ZP, 0xA4}, {AM_ABS, 0xAC}, {AM_ZPX, 0xB4}, {AM_ABSX, 0xBC}});
+  group(mk(U1_PASS, U2_PASS, RG_A, DS_AX, true), CL_READ,
+        {{AM_INDX, 0xA3}, {AM_ZP, 0xA7}, {AM_ABS, 0xAF}, {AM_INDY, 0xB3}, {AM_ZPY, 0xB7}, {AM_ABSY, 0xBF}});
+  group(mk(U1_PASS, U2_CMP, RG_X, DS_NONE, true), CL_READ, {{AM_IMM, 0xE0}, {AM_ZP, 0xE4}, {AM_ABS, 0xEC}});
+  group(mk(U1_PASS, U2_CMP, RG_Y, DS_NONE, true), CL_READ, {{AM_IMM, 0xC0}, {AM_ZP, 0xC4}, {AM_ABS, 0xCC}});
+  group(mk(U1_PASS, U2_BIT, RG_A, DS_NONE, true), CL_READ, {{AM_ZP, 0x24}, {AM_ABS, 0x2C}});
+  // shifts / rotates / inc / dec on memory, and the accumulator forms
+  const uint32_t rmw[6][2] = {{U1_ASL, 0x00}, {U1_ROL, 0x20}, {U1_LSR, 0x40}, {U1_ROR, 0x60},
+                              {U1_DEC, 0xC0}, {U1_INC, 0xE0}};
   for (auto& g : rmw) {
     uint32_t b = g[1];
-    group(g[0], CL_RMW, {{AM_ZP, b + 0x06}, {AM_ABS, b + 0x0E}, {AM_ZPX, b + 0x16}, {AM_ABSX, b + 0x1E}});
-    if (g[0] != OP_DEC && g[0] != OP_INC) put(b + 0x0A, AM_ACC, g[0], 2, false, false);
+    group(mk(g[0], U2_PASS, RG_A, DS_NONE, true), CL_RMW,
+          {{AM_ZP, b + 0x06}, {AM_ABS, b + 0x0E}, {AM_ZPX, b + 0x16}, {AM_ABSX, b + 0x1E}});
+    if (g[0] != U1_DEC && g[0] != U1_INC) {
+      Micro m = mk(g[0], U2_PASS, RG_A, DS_A, true);
+      m.opr = true;
+      table[b + 0x0A] = entry(AM_ACC, 2, false, false, false, m);
+    }
   }
-  // stable undocumented read-modify-write combinations: aaa bbb 11
-  const uint32_t urmw[6][2] = {{OP_SLO, 0x00}, {OP_RLA, 0x20}, {OP_SRE, 0x40}, {OP_RRA, 0x60},
-                               {OP_DCP, 0xC0}, {OP_ISB, 0xE0}};
+  // undocumented RMW combinations (unit1 on memory, unit2 into A)
+  const uint32_t urmw[6][4] = {{U1_ASL, U2_OR, 0x00, DS_A}, {U1_ROL, U2_AND, 0x20, DS_A},
+                               {U1_LSR, U2_EOR, 0x40, DS_A}, {U1_ROR, U2_ADC, 0x60, DS_A},
+                               {U1_DEC, U2_CMP, 0xC0, DS_NONE}, {U1_INC, U2_SBC, 0xE0, DS_A}};
   for (auto& g : urmw) {
-    uint32_t b = g[1];
-    group(g[0], CL_RMW, {{AM_INDX, b + 0x03}, {AM_ZP, b + 0x07}, {AM_ABS, b + 0x0F}, {AM_INDY, b + 0x13},
-                         {AM_ZPX, b + 0x17}, {AM_ABSY, b + 0x1B}, {AM_ABSX, b + 0x1F}});
+    uint32_t b = g[2];
+    group(mk(g[0], g[1], RG_A, g[3], true), CL_RMW,
+          {{AM_INDX, b + 0x03}, {AM_ZP, b + 0x07}, {AM_ABS, b + 0x0F}, {AM_INDY, b + 0x13},
+           {AM_ZPX, b + 0x17}, {AM_ABSY, b + 0x1B}, {AM_ABSX, b + 0x1F}});
   }
-  group(OP_LAX, CL_READ, {{AM_INDX, 0xA3}, {AM_ZP, 0xA7}, {AM_ABS, 0xAF}, {AM_INDY, 0xB3},
-                          {AM_ZPY, 0xB7}, {AM_ABSY, 0xBF}});
-  group(OP_SAX, CL_WRITE, {{AM_INDX, 0x83}, {AM_ZP, 0x87}, {AM_ABS, 0x8F}, {AM_ZPY, 0x97}});
-  group(OP_ANC, CL_READ, {{AM_IMM, 0x0B}, {AM_IMM, 0x2B}});
-  group(OP_ALR, CL_READ, {{AM_IMM, 0x4B}});
-  group(OP_ARR, CL_READ, {{AM_IMM, 0x6B}});
-  group(OP_SBX, CL_READ, {{AM_IMM, 0xCB}});
-  group(OP_SBC, CL_READ, {{AM_IMM, 0xEB}});
-  // NOPs: implied, and the reading NOPs (they perform their data read)
-  for (uint32_t o : {0xEAu, 0x1Au, 0x3Au, 0x5Au, 0x7Au, 0xDAu, 0xFAu}) put(o, AM_IMP, OP_NOP, 2, false, false);
-  group(OP_NOP, CL_READ, {{AM_IMM, 0x80}, {AM_IMM, 0x82}, {AM_IMM, 0x89}, {AM_IMM, 0xC2}, {AM_IMM, 0xE2}});
-  group(OP_NOP, CL_READ, {{AM_ZP, 0x04}, {AM_ZP, 0x44}, {AM_ZP, 0x64}, {AM_ABS, 0x0C}});
-  group(OP_NOP, CL_READ, {{AM_ZPX, 0x14}, {AM_ZPX, 0x34}, {AM_ZPX, 0x54}, {AM_ZPX, 0x74}, {AM_ZPX, 0xD4}, {AM_ZPX, 0xF4}});
-  group(OP_NOP, CL_READ, {{AM_ABSX, 0x1C}, {AM_ABSX, 0x3C}, {AM_ABSX, 0x5C}, {AM_ABSX, 0x7C}, {AM_ABSX, 0xDC}, {AM_ABSX, 0xFC}});
-  // implied register / flag operations
-  const uint32_t impl[][2] = {{0xE8, OP_INX}, {0xC8, OP_INY}, {0xCA, OP_DEX}, {0x88, OP_DEY},
-                              {0xAA, OP_TAX}, {0xA8, OP_TAY}, {0x8A, OP_TXA}, {0x98, OP_TYA},
-                              {0xBA, OP_TSX}, {0x9A, OP_TXS}, {0x18, OP_CLC}, {0x38, OP_SEC},
-                              {0x58, OP_CLI}, {0x78, OP_SEI}, {0xB8, OP_CLV}, {0xD8, OP_CLD},
-                              {0xF8, OP_SED}};
-  for (auto& e : impl) put(e[0], AM_IMP, e[1], 2, false, false);
-  // stack and control flow: fixed counts
-  put(0x48, AM_IMP, OP_PHA, 3, false, false);
-  put(0x08, AM_IMP, OP_PHP, 3, false, false);
-  put(0x68, AM_IMP, OP_PLA, 4, false, false);
-  put(0x28, AM_IMP, OP_PLP, 4, false, false);
-  put(0x4C, AM_ABS, OP_JMP, 3, false, false);
-  put(0x6C, AM_IND, OP_JMP, 5, false, false);
-  put(0x20, AM_ABS, OP_JSR, 6, false, false);
-  put(0x60, AM_IMP, OP_RTS, 6, false, false);
-  put(0x40, AM_IMP, OP_RTI, 6, false, false);
-  put(0x00, AM_IMP, OP_BRK, 7, false, false);
-  // branches: condition flag (N V C Z) in bits 17-18, taken-when-set in bit 19
+  // NOPs (the reading forms perform their data read)
+  Micro nop;
+  for (uint32_t o : {0xEAu, 0x1Au, 0x3Au, 0x5Au, 0x7Au, 0xDAu, 0xFAu}) table[o] = entry(AM_IMP, 2, false, false, false, nop);
+  group(nop, CL_READ, {{AM_IMM, 0x80}, {AM_IMM, 0x82}, {AM_IMM, 0x89}, {AM_IMM, 0xC2}, {AM_IMM, 0xE2},
+                       {AM_ZP, 0x04}, {AM_ZP, 0x44}, {AM_ZP, 0x64}, {AM_ABS, 0x0C},
+                       {AM_ZPX, 0x14}, {AM_ZPX, 0x34}, {AM_ZPX, 0x54}, {AM_ZPX, 0x74}, {AM_ZPX, 0xD4},
+                       {AM_ZPX, 0xF4}, {AM_ABSX, 0x1C}, {AM_ABSX, 0x3C}, {AM_ABSX, 0x5C},
+                       {AM_ABSX, 0x7C}, {AM_ABSX, 0xDC}, {AM_ABSX, 0xFC}});
+  // register increments / transfers: M = R
+  auto reg = [&](uint32_t opc, uint32_t u1, uint32_t rsrc, uint32_t dst, bool nz) {
+    Micro m = mk(u1, U2_PASS, rsrc, dst, nz);
+    m.opr = true;
+    table[opc] = entry(AM_IMP, 2, false, false, false, m);
+  };
+  reg(0xE8, U1_INC, RG_X, DS_X, true);   // INX
+  reg(0xC8, U1_INC, RG_Y, DS_Y, true);   // INY
+  reg(0xCA, U1_DEC, RG_X, DS_X, true);   // DEX
+  reg(0x88, U1_DEC, RG_Y, DS_Y, true);   // DEY
+  reg(0xAA, U1_PASS, RG_A, DS_X, true);  // TAX
+  reg(0xA8, U1_PASS, RG_A, DS_Y, true);  // TAY
+  reg(0x8A, U1_PASS, RG_X, DS_A, true);  // TXA
+  reg(0x98, U1_PASS, RG_Y, DS_A, true);  // TYA
+  reg(0xBA, U1_PASS, RG_SP, DS_X, true); // TSX
+  reg(0x9A, U1_PASS, RG_X, DS_SP, false);// TXS
+  // flag set/clear: (opcode, flag index C=0 I=1 D=2 V=3, value)
+  const uint32_t fl[7][3] = {{0x18, 0, 0}, {0x38, 0, 1}, {0x58, 1, 0}, {0x78, 1, 1},
+                             {0xB8, 3, 0}, {0xD8, 2, 0}, {0xF8, 2, 1}};
+  for (auto& f : fl)
+    table[f[0]] = entry(AM_IMP, 2, false, false, false, nop) | (1ull << dk::FOP) |
+                  ((uint64_t)f[1] << dk::FIDX) | ((uint64_t)f[2] << dk::FVAL);
+  // control flow
+  table[0x4C] = entry(AM_ABS, 3, false, false, false, nop) | (1ull << dk::JMP);
+  table[0x6C] = entry(AM_IND, 5, false, false, false, nop) | (1ull << dk::JMP);
   const uint32_t br[8][3] = {{0x10, 0, 0}, {0x30, 0, 1}, {0x50, 1, 0}, {0x70, 1, 1},
                              {0x90, 2, 0}, {0xB0, 2, 1}, {0xD0, 3, 0}, {0xF0, 3, 1}};
-  for (auto& b : br) table[b[0]] = AM_REL | (OP_BRANCH << 4) | (2u << 11) | (b[1] << 17) | (b[2] << 19);
+  for (auto& b : br)
+    table[b[0]] = entry(AM_REL, 2, false, false, false, nop) | (1ull << dk::BR) |
+                  ((uint64_t)b[1] << dk::BRF) | ((uint64_t)b[2] << dk::BRT);
+  // specials: stack/control and the immediate-only undocumented ops
+  auto spc = [&](uint32_t opc, uint32_t mode, uint32_t cyc, uint32_t s) {
+    table[opc] = entry(mode, cyc, false, false, false, nop) | ((uint64_t)s << dk::SPC);
+  };
+  spc(0x48, AM_IMP, 3, SP_PHA);
+  spc(0x08, AM_IMP, 3, SP_PHP);
+  spc(0x68, AM_IMP, 4, SP_PLA);
+  spc(0x28, AM_IMP, 4, SP_PLP);
+  spc(0x20, AM_ABS, 6, SP_JSR);
+  spc(0x60, AM_IMP, 6, SP_RTS);
+  spc(0x40, AM_IMP, 6, SP_RTI);
+  spc(0x00, AM_IMP, 7, SP_BRK);
+  spc(0x0B, AM_IMM, 2, SP_ANC);
+  spc(0x2B, AM_IMM, 2, SP_ANC);
+  spc(0x4B, AM_IMM, 2, SP_ALR);
+  spc(0x6B, AM_IMM, 2, SP_ARR);
+  spc(0xCB, AM_IMM, 2, SP_SBX);
 }
 
 }  // namespace cule

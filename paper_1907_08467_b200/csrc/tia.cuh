@@ -1,0 +1,397 @@
+// tia.cuh — the video chip (TIA) of one environment, as replayed from its on-chip write log.
+//
+// The CPU loop never touches TIA registers directly: each TIA write is appended, with its
+// colour-clock time T, to a per-environment log in shared memory (the paper's "TIA instruction
+// buffer", kept on-chip instead of in global memory).  The log is replayed
+// ("flushed") by all lanes of a warp together when any lane's log fills, when a frame ends, and
+// — for one lane only — before that lane reads a collision latch.  Replay = for each entry,
+// advance the TIA over [t_tia, T) with the old register values (collisions on every frame,
+// pixels on rendered frames) and then apply the write (DESIGN.md §2 R#4).
+//
+// A span of colour clocks with constant registers is handled per scanline with 160-bit
+// coverage masks (5 x u32 per object): playfield, both players (copies, scaling, reflection),
+// missiles and ball.  Collisions are AND-reductions over the masks; pixels are emitted 4 at a
+// time by byte-selecting the priority-resolved class masks, and packed into 16-byte stores.
+#pragma once
+#include <stdint.h>
+
+namespace cule {
+
+constexpr int kFrameW = 160;
+constexpr int kFrameH = 210;
+constexpr int kFrameBytes = kFrameW * kFrameH;  // 33,600
+constexpr int kFrameChunks = kFrameBytes / 16;  // 2,100
+constexpr int kObs84 = 84 * 84;                 // 7,056
+
+// per-thread shared-memory words, interleaved [word][blockDim] (bank = lane: conflict-free)
+constexpr int kTiaWords = 9;     // TIA registers, positions, collisions, t_tia
+constexpr int kPwWords = 9;      // pixel writer
+constexpr int kLogCap = 32;      // TIA write-log entries per env
+constexpr int kLogMargin = 3;    // an instruction appends at most 3 entries (BRK into TIA space)
+constexpr int kThreadWords = kTiaWords + kPwWords + kLogCap;
+
+// log entry: T (18 bits) << 14 | reg (6 bits) << 8 | value (8 bits)
+__device__ __forceinline__ uint32_t log_entry(uint32_t T, uint32_t reg, uint32_t v) {
+  return (T << 14) | ((reg & 0x3Fu) << 8) | (v & 0xFFu);
+}
+
+__device__ __forceinline__ uint32_t rev8(uint32_t v) { return __brev(v) >> 24; }
+__device__ __forceinline__ uint32_t spread4(uint32_t b) {  // bit k -> bits 4k..4k+3
+  uint32_t x = b & 0xFFu;
+  x = (x | (x << 12)) & 0x000F000Fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  x = (x | (x << 3)) & 0x11111111u;
+  return x * 0xFu;
+}
+__device__ __forceinline__ uint32_t spread2(uint32_t b) {  // bit k -> bits 2k..2k+1
+  uint32_t x = b & 0xFFu;
+  x = (x | (x << 4)) & 0x0F0Fu;
+  x = (x | (x << 2)) & 0x3333u;
+  x = (x | (x << 1)) & 0x5555u;
+  return x * 3u;
+}
+__device__ __forceinline__ uint32_t nib_bytes(uint32_t n) {  // nibble -> 0x00/0xFF byte lanes
+  return (((n & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
+// ---- pixel writer (state in shared memory between flushes) --------------------------------
+struct PixWriter {
+  uint8_t* base;
+  int32_t chunk;
+  uint32_t w0, w1, w2, w3, fill;
+  bool max_mode;
+
+  __device__ __forceinline__ void store_chunk(int32_t c, uint32_t a, uint32_t b, uint32_t d, uint32_t e) {
+    uint4* p = reinterpret_cast<uint4*>(base) + c;
+    if (max_mode) {
+      uint4 o = *p;
+      a = __vmaxu4(a, o.x); b = __vmaxu4(b, o.y); d = __vmaxu4(d, o.z); e = __vmaxu4(e, o.w);
+    }
+    *p = make_uint4(a, b, d, e);
+  }
+  __device__ __forceinline__ void advance_to(int32_t c) {
+    if (chunk >= 0) store_chunk(chunk, w0, w1, w2, w3);
+    if (!(max_mode && fill == 0))
+      for (int32_t k = chunk + 1; k < c; ++k) store_chunk(k, fill, fill, fill, fill);
+    chunk = c;
+    w0 = w1 = w2 = w3 = fill;
+  }
+  __device__ __forceinline__ void put(int32_t g, uint32_t px, uint32_t bmask) {
+    int32_t c = g >> 2;
+    if (c != chunk) advance_to(c);
+    switch (g & 3) {
+      case 0: w0 = (w0 & ~bmask) | (px & bmask); break;
+      case 1: w1 = (w1 & ~bmask) | (px & bmask); break;
+      case 2: w2 = (w2 & ~bmask) | (px & bmask); break;
+      default: w3 = (w3 & ~bmask) | (px & bmask); break;
+    }
+  }
+  __device__ __forceinline__ void load(const uint32_t* w, uint32_t s) {
+    base = reinterpret_cast<uint8_t*>((uint64_t)w[0] | ((uint64_t)w[s] << 32));
+    chunk = (int32_t)w[2 * s];
+    w0 = w[3 * s]; w1 = w[4 * s]; w2 = w[5 * s]; w3 = w[6 * s];
+    fill = w[7 * s];
+    max_mode = (w[8 * s] & 2u) != 0;
+  }
+  __device__ __forceinline__ void save(uint32_t* w, uint32_t s) const {
+    w[2 * s] = (uint32_t)chunk;
+    w[3 * s] = w0; w[4 * s] = w1; w[5 * s] = w2; w[6 * s] = w3;
+  }
+};
+
+// begin rendering a frame: writer state in shared memory (flags bit0 = render, bit1 = max)
+__device__ __forceinline__ void pw_begin(uint32_t* w, uint32_t s, uint8_t* base, uint32_t fill4, bool mx) {
+  const uint64_t b = reinterpret_cast<uint64_t>(base);
+  w[0] = (uint32_t)b; w[s] = (uint32_t)(b >> 32);
+  w[2 * s] = 0xFFFFFFFFu;  // chunk -1
+  w[3 * s] = w[4 * s] = w[5 * s] = w[6 * s] = fill4;
+  w[7 * s] = fill4;
+  w[8 * s] = 1u | (mx ? 2u : 0u);
+}
+__device__ __forceinline__ bool pw_rendering(const uint32_t* w, uint32_t s) { return (w[8 * s] & 1u) != 0; }
+__device__ __forceinline__ void pw_end(uint32_t* w, uint32_t s) {
+  PixWriter pw;
+  pw.load(w, s);
+  pw.advance_to(kFrameChunks);
+  w[8 * s] = 0u;
+}
+__device__ __forceinline__ void pw_stop(uint32_t* w, uint32_t s) { w[8 * s] = 0u; }
+
+// ---- TIA register file (registers while replaying) ------------------------------------------
+struct Tia {
+  uint32_t colup0, colup1, colupf, colubk, pf0, pf1, pf2, ctrlpf;
+  uint32_t nusiz0, nusiz1, grp0n, grp0o, grp1n, grp1o, hmp0, hmp1, hmm0, hmm1, hmbl;
+  uint32_t flags;  // bit 0 vblank, 1 refp0, 2 refp1, 3 enam0, 4 enam1, 5 enbln, 6 enblo,
+                   // 7 vdelp0, 8 vdelp1, 9 vdelbl, 10 resmp0, 11 resmp1
+  int32_t comb_line;
+  uint32_t posP0, posP1, posM0, posM1, posBL;
+  uint32_t coll;
+  uint32_t t_tia;
+
+  __device__ __forceinline__ uint32_t f(int b) const { return (flags >> b) & 1u; }
+  __device__ __forceinline__ void setf(int b, uint32_t v) { flags = (flags & ~(1u << b)) | ((v & 1u) << b); }
+
+  __device__ __forceinline__ void load(const uint32_t* w, uint32_t s) {
+    uint32_t a = w[0], b = w[s], c = w[2 * s], d = w[3 * s], e = w[4 * s], g = w[5 * s], h = w[6 * s],
+             k = w[7 * s];
+    colup0 = a & 0xFF; colup1 = (a >> 8) & 0xFF; colupf = (a >> 16) & 0xFF; colubk = a >> 24;
+    pf0 = b & 0xFF; pf1 = (b >> 8) & 0xFF; pf2 = (b >> 16) & 0xFF; ctrlpf = b >> 24;
+    nusiz0 = c & 0xFF; nusiz1 = (c >> 8) & 0xFF; grp0n = (c >> 16) & 0xFF; grp0o = c >> 24;
+    grp1n = d & 0xFF; grp1o = (d >> 8) & 0xFF; hmp0 = (d >> 16) & 0xFF; hmp1 = d >> 24;
+    hmm0 = e & 0xFF; hmm1 = (e >> 8) & 0xFF; hmbl = (e >> 16) & 0xFF;
+    flags = g & 0xFFFF; comb_line = (int32_t)(int16_t)(g >> 16);
+    posP0 = h & 0xFF; posP1 = (h >> 8) & 0xFF; posM0 = (h >> 16) & 0xFF; posM1 = h >> 24;
+    posBL = k & 0xFF; coll = k >> 16;
+    t_tia = w[8 * s];
+  }
+  __device__ __forceinline__ void store(uint32_t* w, uint32_t s) const {
+    w[0] = colup0 | (colup1 << 8) | (colupf << 16) | (colubk << 24);
+    w[s] = pf0 | (pf1 << 8) | (pf2 << 16) | (ctrlpf << 24);
+    w[2 * s] = nusiz0 | (nusiz1 << 8) | (grp0n << 16) | (grp0o << 24);
+    w[3 * s] = grp1n | (grp1o << 8) | (hmp0 << 16) | (hmp1 << 24);
+    w[4 * s] = hmm0 | (hmm1 << 8) | (hmbl << 16);
+    w[5 * s] = (flags & 0xFFFF) | ((uint32_t)(comb_line & 0xFFFF) << 16);
+    w[6 * s] = posP0 | (posP1 << 8) | (posM0 << 16) | (posM1 << 24);
+    w[7 * s] = posBL | (coll << 16);
+    w[8 * s] = t_tia;
+  }
+
+  struct Masks { uint32_t p0[5], p1[5], m0[5], m1[5], bl[5], pf[5]; };
+
+  __device__ __forceinline__ static void place(uint32_t* m, uint32_t pat, uint32_t p) {
+    uint32_t wi = p >> 5, s = p & 31;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      if (k == (int)wi) m[k] |= pat << s;
+      if (s && k == (int)(wi == 4 ? 0 : wi + 1)) m[k] |= pat >> (32 - s);
+    }
+  }
+  // NUSIZ copy set: bit0 +0, bit1 +16, bit2 +32, bit3 +64
+  __device__ __forceinline__ static uint32_t copies(uint32_t mode) { return (0x1D197531u >> (4 * mode)) & 0xF; }
+  __device__ __forceinline__ static void player_mask(uint32_t* m, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) m[k] = 0;
+    if (g == 0) return;
+    uint32_t mode = nusiz & 7;
+    uint32_t pat = refl ? g : rev8(g);
+    if (mode == 5) pat = spread2(pat);
+    else if (mode == 7) pat = spread4(pat);
+    uint32_t cp = copies(mode);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (cp & (1u << c)) {
+        uint32_t p = pos + (c == 0 ? 0u : (8u << c));
+        place(m, pat, p >= 160u ? p - 160u : p);
+      }
+  }
+  __device__ __forceinline__ static void missile_mask(uint32_t* m, uint32_t pos, uint32_t nusiz, bool en) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) m[k] = 0;
+    if (!en) return;
+    uint32_t mode = nusiz & 7;
+    uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3))) - 1u;
+    uint32_t cp = (mode == 5 || mode == 7) ? 1u : copies(mode);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (cp & (1u << c)) {
+        uint32_t p = pos + (c == 0 ? 0u : (8u << c));
+        place(m, pat, p >= 160u ? p - 160u : p);
+      }
+  }
+  __device__ __forceinline__ void build_masks(Masks& M) const {
+    player_mask(M.p0, posP0, nusiz0, f(7) ? grp0o : grp0n, f(1));
+    player_mask(M.p1, posP1, nusiz1, f(8) ? grp1o : grp1n, f(2));
+    missile_mask(M.m0, posM0, nusiz0, f(3) && !f(10));
+    missile_mask(M.m1, posM1, nusiz1, f(4) && !f(11));
+#pragma unroll
+    for (int k = 0; k < 5; ++k) M.bl[k] = 0;
+    if (f(9) ? f(6) : f(5)) place(M.bl, (1u << (1u << ((ctrlpf >> 4) & 3))) - 1u, posBL);
+    uint32_t left = ((pf0 >> 4) & 0xF) | (rev8(pf1) << 4) | ((pf2 & 0xFF) << 12);
+    uint32_t right = (ctrlpf & 1) ? (__brev(left) >> 12) : left;
+    uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) M.pf[k] = spread4((uint32_t)(cells >> (8 * k)));
+  }
+
+  // OR the collision latches of visible pixels [xa, xb) (bit 2r = d7, 2r+1 = d6 of register r)
+  __device__ __forceinline__ void collide(const Masks& M, uint32_t xa, uint32_t xb) {
+    uint32_t a00 = 0, a01 = 0, a02 = 0, a03 = 0, a04 = 0, a05 = 0, a06 = 0, a07 = 0, a08 = 0, a09 = 0,
+             a10 = 0, a11 = 0, a12 = 0, a14 = 0, a15 = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      uint32_t lo = 32u * k;
+      uint32_t s = xa > lo ? min(xa - lo, 32u) : 0u, e = xb > lo ? min(xb - lo, 32u) : 0u;
+      uint32_t r = e > s ? ((e - s == 32u ? 0xFFFFFFFFu : ((1u << (e - s)) - 1u)) << s) : 0u;
+      uint32_t p0 = M.p0[k] & r, p1 = M.p1[k] & r, m0 = M.m0[k] & r, m1 = M.m1[k] & r,
+               bl = M.bl[k] & r, pf = M.pf[k] & r;
+      a00 |= m0 & p1; a01 |= m0 & p0; a02 |= m1 & p0; a03 |= m1 & p1;
+      a04 |= p0 & pf; a05 |= p0 & bl; a06 |= p1 & pf; a07 |= p1 & bl;
+      a08 |= m0 & pf; a09 |= m0 & bl; a10 |= m1 & pf; a11 |= m1 & bl;
+      a12 |= bl & pf; a14 |= p0 & p1; a15 |= m0 & m1;
+    }
+    coll |= (a00 ? 1u : 0u) | (a01 ? 2u : 0u) | (a02 ? 4u : 0u) | (a03 ? 8u : 0u) |
+            (a04 ? 0x10u : 0u) | (a05 ? 0x20u : 0u) | (a06 ? 0x40u : 0u) | (a07 ? 0x80u : 0u) |
+            (a08 ? 0x100u : 0u) | (a09 ? 0x200u : 0u) | (a10 ? 0x400u : 0u) | (a11 ? 0x800u : 0u) |
+            (a12 ? 0x1000u : 0u) | (a14 ? 0x4000u : 0u) | (a15 ? 0x8000u : 0u);
+  }
+
+  __device__ __forceinline__ static uint32_t shade(uint32_t colu, const uint8_t* gray) {
+    uint32_t idx = (colu >> 1) & 0x7F;
+    return (gray ? (uint32_t)gray[idx] : idx) * 0x01010101u;
+  }
+
+  __device__ __forceinline__ void render_span(const Masks& M, PixWriter& pw, uint32_t line, uint32_t row,
+                                              uint32_t xa, uint32_t xb, const uint8_t* gray) {
+    uint32_t cbk = shade(colubk, gray), c0 = shade(colup0, gray), c1 = shade(colup1, gray),
+             cbl = shade(colupf, gray);
+    uint32_t cpl = (ctrlpf & 2) ? c0 : cbl, cpr = (ctrlpf & 2) ? c1 : cbl;
+    bool pfp = ctrlpf & 4;
+    bool comb = (int32_t)line == comb_line;
+    uint32_t base_g = row * (kFrameW / 4);
+    for (uint32_t g = xa >> 2; g <= (xb - 1) >> 2; ++g) {
+      uint32_t k = g >> 3, sh = (g & 7) * 4;
+      uint32_t q0 = 0, q1 = 0, qb = 0, qp = 0;
+#pragma unroll
+      for (int kk = 0; kk < 5; ++kk)
+        if (kk == (int)k) {
+          q0 = M.p0[kk] | M.m0[kk]; q1 = M.p1[kk] | M.m1[kk]; qb = M.bl[kk]; qp = M.pf[kk];
+        }
+      uint32_t np0 = (q0 >> sh) & 0xF, np1 = (q1 >> sh) & 0xF, nbl = (qb >> sh) & 0xF, npf = (qp >> sh) & 0xF;
+      uint32_t e0, e1, eb, ep;
+      if (!pfp) {
+        e0 = np0; e1 = np1 & ~e0; eb = nbl & ~(e0 | e1); ep = npf & ~(e0 | e1 | nbl);
+      } else {
+        eb = nbl; ep = npf & ~nbl; e0 = np0 & ~(nbl | npf); e1 = np1 & ~(nbl | npf | np0);
+      }
+      uint32_t B0 = nib_bytes(e0), B1 = nib_bytes(e1), Bb = nib_bytes(eb), Bp = nib_bytes(ep);
+      uint32_t cp = g < 20 ? cpl : cpr;
+      uint32_t px = (c0 & B0) | (c1 & B1) | (cbl & Bb) | (cp & Bp) | (cbk & ~(B0 | B1 | Bb | Bp));
+      if (comb && g < 2) px = pw.fill;
+      uint32_t x0 = g * 4;
+      uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 4 ? xb - x0 : 4u;
+      uint32_t bm = (0xFFFFFFFFu >> (32 - 8 * (hi - lo))) << (8 * lo);
+      pw.put((int32_t)(base_g + g), px, bm);
+    }
+  }
+  __device__ __forceinline__ static void render_black(PixWriter& pw, uint32_t row, uint32_t xa, uint32_t xb) {
+    uint32_t base_g = row * (kFrameW / 4);
+    for (uint32_t g = xa >> 2; g <= (xb - 1) >> 2; ++g) {
+      uint32_t x0 = g * 4;
+      uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 4 ? xb - x0 : 4u;
+      uint32_t bm = (0xFFFFFFFFu >> (32 - 8 * (hi - lo))) << (8 * lo);
+      pw.put((int32_t)(base_g + g), pw.fill, bm);
+    }
+  }
+
+  // advance over colour clocks [t_tia, t_to)
+  __device__ __forceinline__ void catch_up(uint32_t t_to, bool render, PixWriter& pw, uint32_t ystart,
+                                           const uint8_t* gray) {
+    uint32_t t0 = t_tia;
+    if (t_to <= t0) return;
+    t_tia = t_to;
+    uint32_t l0 = t0 / 228u, l1 = (t_to - 1) / 228u;
+    bool have = false, full_done = false;
+    Masks M;
+    for (uint32_t ln = l0; ln <= l1; ++ln) {
+      uint32_t h0 = (ln == l0) ? t0 - ln * 228u : 0u;
+      uint32_t h1 = (ln == l1) ? t_to - ln * 228u : 228u;
+      if (h1 <= 68u) continue;
+      uint32_t xa = h0 > 68u ? h0 - 68u : 0u, xb = h1 - 68u;
+      bool inwin = render && ln >= ystart && ln < ystart + (uint32_t)kFrameH;
+      if (f(0)) {  // VBLANK: black, no collisions
+        if (inwin) render_black(pw, ln - ystart, xa, xb);
+        continue;
+      }
+      if (!have) { build_masks(M); have = true; }
+      bool full = xa == 0 && xb == 160u;
+      if (!(full && full_done)) collide(M, xa, xb);
+      if (full) full_done = true;
+      if (inwin) render_span(M, pw, ln, ln - ystart, xa, xb, gray);
+    }
+  }
+
+  // apply a logged write at colour clock T (WSYNC/VSYNC/RSYNC/audio never reach the log)
+  __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T) {
+    uint32_t line = T / 228u, h = T - line * 228u;
+    int32_t hp = (int32_t)h - 68;
+    switch (r) {
+      case 0x01: setf(0, (v >> 1) & 1); break;
+      case 0x04: nusiz0 = v; break;
+      case 0x05: nusiz1 = v; break;
+      case 0x06: colup0 = v; break;
+      case 0x07: colup1 = v; break;
+      case 0x08: colupf = v; break;
+      case 0x09: colubk = v; break;
+      case 0x0A: ctrlpf = v; break;
+      case 0x0B: setf(1, v >> 3); break;
+      case 0x0C: setf(2, v >> 3); break;
+      case 0x0D: pf0 = v; break;
+      case 0x0E: pf1 = v; break;
+      case 0x0F: pf2 = v; break;
+      case 0x10: case 0x11: case 0x12: case 0x13: case 0x14: {
+        uint32_t base = r <= 0x11 ? 5u : 4u;
+        uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
+        if (r == 0x10) posP0 = p; else if (r == 0x11) posP1 = p;
+        else if (r == 0x12) posM0 = p; else if (r == 0x13) posM1 = p; else posBL = p;
+      } break;
+      case 0x1B: grp0n = v; grp1o = grp1n; break;
+      case 0x1C: grp1n = v; grp0o = grp0n; setf(6, f(5)); break;
+      case 0x1D: setf(3, v >> 1); break;
+      case 0x1E: setf(4, v >> 1); break;
+      case 0x1F: setf(5, v >> 1); break;
+      case 0x20: hmp0 = v >> 4; break;
+      case 0x21: hmp1 = v >> 4; break;
+      case 0x22: hmm0 = v >> 4; break;
+      case 0x23: hmm1 = v >> 4; break;
+      case 0x24: hmbl = v >> 4; break;
+      case 0x25: setf(7, v); break;
+      case 0x26: setf(8, v); break;
+      case 0x27: setf(9, v); break;
+      case 0x28: case 0x29: {
+        const int b = r == 0x28 ? 10 : 11;
+        uint32_t nv = (v >> 1) & 1;
+        if (f(b) && !nv) {
+          uint32_t md = (r == 0x28 ? nusiz0 : nusiz1) & 7;
+          uint32_t c = md == 5 ? 6u : (md == 7 ? 10u : 3u);
+          if (r == 0x28) posM0 = (posP0 + c) % 160u; else posM1 = (posP1 + c) % 160u;
+        }
+        setf(b, nv);
+      } break;
+      case 0x2A: {
+        auto mv = [](uint32_t p, uint32_t hm) -> uint32_t {
+          int32_t q = (int32_t)p - ((int32_t)(hm ^ 8u) - 8);
+          return (uint32_t)(q < 0 ? q + 160 : (q >= 160 ? q - 160 : q));
+        };
+        posP0 = mv(posP0, hmp0); posP1 = mv(posP1, hmp1); posM0 = mv(posM0, hmm0);
+        posM1 = mv(posM1, hmm1); posBL = mv(posBL, hmbl);
+        if (h < 68u) comb_line = (int32_t)line;
+      } break;
+      case 0x2B: hmp0 = hmp1 = hmm0 = hmm1 = hmbl = 0; break;
+      case 0x2C: coll = 0; break;
+      default: break;
+    }
+  }
+};
+
+// Replay n log entries of this lane, then (optionally) advance to t_final.
+// tw: this thread's TIA words, pw_w: pixel-writer words, lg: log words (all stride s).
+__device__ __forceinline__ void flush_lane(uint32_t* tw, uint32_t* pw_w, const uint32_t* lg, uint32_t s,
+                                           uint32_t n, bool final_catch, uint32_t t_final, uint32_t ystart,
+                                           const uint8_t* gray) {
+  Tia t;
+  t.load(tw, s);
+  PixWriter pw;
+  const bool render = pw_rendering(pw_w, s);
+  if (render) pw.load(pw_w, s);
+  for (uint32_t k = 0; k < n; ++k) {
+    uint32_t e = lg[k * s];
+    uint32_t T = e >> 14;
+    t.catch_up(T, render, pw, ystart, gray);
+    t.apply((e >> 8) & 0x3Fu, e & 0xFFu, T);
+  }
+  if (final_catch) t.catch_up(t_final, render, pw, ystart, gray);
+  t.store(tw, s);
+  if (render) pw.save(pw_w, s);
+}
+
+}  // namespace cule
