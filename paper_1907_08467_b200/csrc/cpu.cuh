@@ -16,10 +16,15 @@ enum Event : uint32_t { EV_NONE = 0, EV_LOGFULL = 1, EV_FRAME = 2, EV_FAULT = 3 
 
 // out-of-line so the rare collision-read path does not bloat the hot loop; scalar arguments
 // only, so no caller state is forced into local memory
-__device__ __noinline__ uint32_t coll_read_flush(uint32_t* tw, uint32_t* pw, const uint32_t* lg, uint32_t s,
-                                                 uint32_t n, uint32_t t, uint32_t ystart, const uint8_t* gray) {
-  flush_lane(tw, pw, lg, s, n, true, t, ystart, gray);
-  return tw[7 * s] >> 16;
+__device__ __noinline__ uint32_t flush_call(uint32_t* tw, uint32_t* pw, const uint32_t* lg, uint32_t s,
+                                            uint32_t n, uint32_t fin, uint32_t t, uint32_t ystart,
+                                            const uint8_t* gray) {
+  flush_lane(tw, pw, lg, s, n, fin != 0, t, ystart, gray);
+  return tw[7 * s] >> 16;  // collision latches
+}
+__device__ __forceinline__ uint32_t coll_read_flush(uint32_t* tw, uint32_t* pw, const uint32_t* lg, uint32_t s,
+                                                    uint32_t n, uint32_t t, uint32_t ystart, const uint8_t* gray) {
+  return flush_call(tw, pw, lg, s, n, 1u, t, ystart, gray);
 }
 
 struct Ctx {
@@ -34,6 +39,7 @@ struct Ctx {
   uint32_t* lg;           // this thread's TIA write log
   uint32_t s;             // word stride = blockDim
   uint32_t ystart, line_cap;
+  uint32_t cap_cycles;    // 76 * line_cap
 };
 
 struct Cpu {
@@ -238,7 +244,7 @@ struct Cpu {
     fc = now;
     t_phaseA = 3u * now;
     if (wsync_pending) fc = ((fc + 75u) / 76u) * 76u;  // stall to the next line start (R#5)
-    if (fc / 76u >= c.line_cap) { fault = 2; return EV_FAULT; }
+    if (fc >= c.cap_cycles) { fault = 2; return EV_FAULT; }  // fc / 76 >= line_cap
     if (vsync_rose) return EV_FRAME;
     return log_len > (uint32_t)(kLogCap - kLogMargin) ? EV_LOGFULL : EV_NONE;
   }

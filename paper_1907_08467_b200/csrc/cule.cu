@@ -45,11 +45,11 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
   L->state = take(256 * n);
   L->pack = take(256 * n);
-  L->staging = take(gray ? n * cule::kFrameBytes : 0);
+  L->staging = take(gray ? 2 * n * cule::kFrameBytes : 0);  // frames fs-1 and fs per env
   L->cstate = take(256 * nk);
   L->cobs = take(nk * ob);
   L->cscore = take(2 * nk);
-  L->cstage = take(gray ? nk * cule::kFrameBytes : 0);
+  L->cstage = take(gray ? 2 * nk * cule::kFrameBytes : 0);
   L->roms = take(4 * 8192);
   L->decode = take(2048);
   L->gray = take(128);
@@ -76,6 +76,9 @@ struct cule_env {
   uint64_t pick_seed;
   size_t smem;
   uint32_t block;
+  uint32_t epw;            // envs per warp
+  uint32_t slot_start[4], first_env[4];
+  uint32_t grid;           // blocks of the step / debug kernels
 };
 
 static cule::Params base_params(const cule_env* e) {
@@ -112,6 +115,8 @@ static cule::Params base_params(const cule_env* e) {
   p.cache_score_out = reinterpret_cast<uint16_t*>(e->ws + e->L.cscore);
   p.cache_staging = e->ws + e->L.cstage;
   p.error_flag = reinterpret_cast<int32_t*>(e->ws + e->L.err);
+  p.epw = e->epw;
+  for (int r = 0; r < 4; ++r) { p.slot_start[r] = e->slot_start[r]; p.first_env[r] = e->first_env[r]; }
   return p;
 }
 
@@ -131,18 +136,36 @@ static int cuda_check(const char* what) {
 
 static constexpr int kMaxBlock = 128;
 
-// threads per block: small blocks spread few envs over all SMs (the low-env regime is
-// latency-bound); CULE_BLOCK overrides (32, 64 or 128)
-static uint32_t choose_block(int N) {
+static int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// Envs per warp: the per-env 6502 chain is latency-bound, so at low env counts the kernel
+// uses fewer lanes per warp (more warps, less divergence) until each SM sub-partition has a
+// few warps to switch between.  CULE_EPW overrides (1..32, power of two).
+static uint32_t choose_epw(int N) {
+  if (const char* v = getenv("CULE_EPW")) {
+    int b = atoi(v);
+    if (b >= 1 && b <= 32 && (b & (b - 1)) == 0) return (uint32_t)b;
+  }
+  // measured on B200 (profiles/r01_*): 4096 envs peak at 4-8 envs/warp, 32K envs at 32
+  const uint32_t target_warps = 6u * (uint32_t)sm_count();
+  uint32_t e = 32;
+  while (e > 1 && ((uint32_t)N + e - 1) / e < target_warps) e /= 2;
+  return e;
+}
+
+// threads per block: small blocks spread few warps over all SMs; CULE_BLOCK overrides
+static uint32_t choose_block(uint32_t warps) {
   if (const char* v = getenv("CULE_BLOCK")) {
     int b = atoi(v);
     if (b == 32 || b == 64 || b == 128) return (uint32_t)b;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   uint32_t b = 128;
-  while (b > 32 && ((uint32_t)N + b - 1) / b < 2u * (uint32_t)sms) b /= 2;
+  while (b > 32 && (warps * 32u + b - 1) / b < 2u * (uint32_t)sm_count()) b /= 2;
   return b;
 }
 
@@ -222,7 +245,22 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     if (rom_lens[r] == 8192) e->f8_mask |= 1u << r;
   }
   e->rom_bytes = off;
-  e->block = choose_block(num_envs);
+  e->epw = choose_epw(num_envs);
+  {
+    const uint32_t warps = ((uint32_t)num_envs + e->epw - 1) / e->epw;
+    e->block = choose_block(warps);
+    e->grid = (warps * 32u + e->block - 1) / e->block;
+    uint32_t slot = 0;
+    for (int r = 0; r < 4; ++r) { e->slot_start[r] = 0; e->first_env[r] = 0; }
+    for (int r = 0; r < n_roms; ++r) {
+      const int64_t base = cfg->env_index_base;
+      const uint32_t first = (uint32_t)((((int64_t)r - base) % n_roms + n_roms) % n_roms);
+      const uint32_t cnt = first < (uint32_t)num_envs ? ((uint32_t)num_envs - first + n_roms - 1) / n_roms : 0u;
+      e->slot_start[r] = slot;
+      e->first_env[r] = first;
+      slot += cnt;
+    }
+  }
   e->smem = cule::smem_bytes(e->rom_bytes, e->block);
   const size_t smem_max = cule::smem_bytes(e->rom_bytes, kMaxBlock);
 
@@ -301,9 +339,8 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
   p.obs = static_cast<uint8_t*>(d_obs);
   p.rewards = d_rewards;
   p.dones = d_dones;
-  const uint32_t blocks = ((uint32_t)e->N + e->block - 1) / e->block;
-  if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::step_kernel<true><<<blocks, e->block, e->smem, s>>>(p);
-  else cule::step_kernel<false><<<blocks, e->block, e->smem, s>>>(p);
+  if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::step_kernel<true><<<e->grid, e->block, e->smem, s>>>(p);
+  else cule::step_kernel<false><<<e->grid, e->block, e->smem, s>>>(p);
   return cuda_check("step_kernel");
 }
 
@@ -370,8 +407,7 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
   cule::Params p = base_params(e);
   p.debug_instr = n_instr;
   p.debug_status = d_status;
-  const uint32_t blocks = ((uint32_t)e->N + e->block - 1) / e->block;
-  cule::debug_kernel<<<blocks, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
+  cule::debug_kernel<<<e->grid, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
   return cuda_check("debug_kernel");
 }
 

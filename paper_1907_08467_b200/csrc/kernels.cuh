@@ -52,7 +52,26 @@ struct Params {
   uint16_t* cache_score_out;
   uint8_t* cache_staging;
   int32_t* error_flag;
+  // thread -> env mapping: `epw` envs per warp (lanes >= epw idle), slots grouped by ROM
+  uint32_t epw;
+  uint32_t slot_start[4];   // first slot of ROM r
+  uint32_t first_env[4];    // first local env of ROM r (envs of ROM r are first_env[r] + n_roms*k)
 };
+
+// The env a thread emulates.  Envs are laid out so that the lanes of a warp run the same ROM
+// (g % n_roms), and at most `epw` lanes of a warp are used: at low env counts fewer envs per
+// warp means more warps to hide latency and less divergence per warp.
+__device__ __forceinline__ bool env_of_thread(const Params& p, uint32_t& i) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t l = t & 31u;
+  if (l >= p.epw) return false;
+  const uint32_t s = (t >> 5) * p.epw + l;
+  if (s >= p.N) return false;
+  uint32_t r = 0;
+  while (r + 1 < p.n_roms && s >= p.slot_start[r + 1]) ++r;
+  i = p.first_env[r] + p.n_roms * (s - p.slot_start[r]);
+  return true;
+}
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -116,6 +135,7 @@ __device__ __forceinline__ Ctx stage_block(const Params& p, uint8_t* smem, bool 
   c.lg = words + (kTiaWords + kPwWords) * blockDim.x + threadIdx.x;
   c.ystart = p.ystart;
   c.line_cap = p.line_cap;
+  c.cap_cycles = 76u * p.line_cap;
   return c;
 }
 
@@ -253,7 +273,8 @@ __device__ __forceinline__ int32_t simulate(Cpu& m, const Ctx& c, bool active, u
   auto begin_frame = [&]() {
     ++f;
     render = !kDebug && (kGray ? (f + 1 >= nframes) : (f == nframes));
-    if (render) pw_begin(c.pw, c.s, frame_out, fill, kGray && f == nframes && nframes >= 2);
+    // GRAY: frame fs-1 -> first half of the env's staging pair, frame fs -> second half
+    if (render) pw_begin(c.pw, c.s, (kGray && f == nframes) ? frame_out + kFrameBytes : frame_out, fill);
     if (episode_frames) ++*episode_frames;
   };
   if (running) begin_frame();
@@ -269,7 +290,7 @@ __device__ __forceinline__ int32_t simulate(Cpu& m, const Ctx& c, bool active, u
     }
     if (__any_sync(kFull, ev != EV_NONE)) {
       const bool fin = ev == EV_FRAME || ev == EV_FAULT || ev == EV_BUDGET;
-      if (m.log_len || fin) flush_lane(c.tw, c.pw, c.lg, c.s, m.log_len, fin, 3u * m.fc, c.ystart, c.gray);
+      if (m.log_len || fin) flush_call(c.tw, c.pw, c.lg, c.s, m.log_len, fin ? 1u : 0u, 3u * m.fc, c.ystart, c.gray);
       m.log_len = 0;
       if (ev == EV_FRAME) {
         end_frame(m, c);
@@ -293,7 +314,12 @@ __device__ __forceinline__ int32_t simulate(Cpu& m, const Ctx& c, bool active, u
 // ---- warp-cooperative area84 ------------------------------------------------------------------
 // out[i][j] = round_half_even(sum wr(i,r) wc(j,c) f[r][c] / 200): exact overlap weights of
 // 210->84 rows (units 2 vs 5) and 160->84 columns (units 21 vs 40) (§8(c).12)
-__device__ __forceinline__ void warp_area84(const uint8_t* f, uint8_t* out, uint32_t lane) {
+// m = max(fa, fb) pixel-wise (fb may be null: single frame)
+__device__ __forceinline__ uint32_t px_max(const uint8_t* fa, const uint8_t* fb, uint32_t o) {
+  const uint32_t a = fa[o];
+  return fb ? max(a, (uint32_t)fb[o]) : a;
+}
+__device__ __forceinline__ void warp_area84(const uint8_t* fa, const uint8_t* fb, uint8_t* out, uint32_t lane) {
   for (uint32_t j = lane; j < 84u; j += 32u) {
     const uint32_t a = 40u * j, b = a + 40u;
     const uint32_t c0 = a / 21u;
@@ -303,12 +329,12 @@ __device__ __forceinline__ void warp_area84(const uint8_t* f, uint8_t* out, uint
     for (uint32_t i = 0; i < 84u; ++i) {
       const uint32_t r0 = (i >> 1) * 5u + ((i & 1u) ? 2u : 0u);
       const uint32_t w0 = (i & 1u) ? 1u : 2u, w2 = (i & 1u) ? 2u : 1u;
-      const uint8_t* p = f + r0 * 160u + c0;
-      uint32_t s0 = wc0 * p[0] + wc1 * p[1] + (wc2 ? wc2 * p[2] : 0u);
-      p += 160;
-      uint32_t s1 = wc0 * p[0] + wc1 * p[1] + (wc2 ? wc2 * p[2] : 0u);
-      p += 160;
-      uint32_t s2 = wc0 * p[0] + wc1 * p[1] + (wc2 ? wc2 * p[2] : 0u);
+      uint32_t o = r0 * 160u + c0;
+      uint32_t s0 = wc0 * px_max(fa, fb, o) + wc1 * px_max(fa, fb, o + 1) + (wc2 ? wc2 * px_max(fa, fb, o + 2) : 0u);
+      o += 160;
+      uint32_t s1 = wc0 * px_max(fa, fb, o) + wc1 * px_max(fa, fb, o + 1) + (wc2 ? wc2 * px_max(fa, fb, o + 2) : 0u);
+      o += 160;
+      uint32_t s2 = wc0 * px_max(fa, fb, o) + wc1 * px_max(fa, fb, o + 1) + (wc2 ? wc2 * px_max(fa, fb, o + 2) : 0u);
       const uint32_t S = w0 * s0 + 2u * s1 + w2 * s2;
       uint32_t q = S / 200u;
       const uint32_t r = S - 200u * q;
@@ -327,9 +353,9 @@ template <bool kGray>
 __global__ void __launch_bounds__(128) step_kernel(Params p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const Ctx c = stage_block(p, smem, kGray);
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t i = 0;
+  const bool active = env_of_thread(p, i);
   const uint32_t lane = threadIdx.x & 31u;
-  const bool active = i < p.N;
   const size_t N = p.N;
   uint4* st = reinterpret_cast<uint4*>(p.state);
   Cpu m{};
@@ -346,7 +372,7 @@ __global__ void __launch_bounds__(128) step_kernel(Params p) {
     const uint4 bk = st[12 * N + i];
     episode_frames = bk.x; episode_index = bk.y; episode_return = (int32_t)bk.z; prev_score = bk.w & 0xFFFFu;
     set_inputs(m, p.actions[i]);
-    frame_out = (kGray ? p.staging : p.obs) + (size_t)i * kFrameBytes;
+    frame_out = kGray ? p.staging + (size_t)i * (2 * kFrameBytes) : p.obs + (size_t)i * kFrameBytes;
   }
   const int32_t status = simulate<kGray, false>(m, c, active, p.fs, frame_out, &episode_frames, 0);
   uint32_t fault = 0, done = 0, ep_ret_done = 0;
@@ -397,15 +423,18 @@ __global__ void __launch_bounds__(128) step_kernel(Params p) {
     if (n_fault) atomicAdd(&p.counters[3], (unsigned long long)n_fault);
   }
   // a5: warp-cooperative observation epilogue
-  const uint32_t warp_base = i - lane;
   for (uint32_t l = 0; l < 32u; ++l) {
     if (!((amask >> l) & 1u)) continue;
-    const uint32_t env = warp_base + l;
+    const uint32_t env = __shfl_sync(kFull, i, l);
     const uint32_t f = __shfl_sync(kFull, fault, l);
     if (kGray) {
       uint8_t* o = p.obs + (size_t)env * kObs84;
       if (f) warp_zero(o, kObs84, lane);
-      else warp_area84(p.staging + (size_t)env * kFrameBytes, o, lane);
+      else {
+        const uint8_t* pair = p.staging + (size_t)env * (2 * kFrameBytes);
+        // fs >= 2: max of frames fs-1 (first half) and fs (second half); fs == 1: frame fs only
+        warp_area84(pair + kFrameBytes, p.fs >= 2 ? pair : nullptr, o, lane);
+      }
     } else if (f) {
       warp_zero(p.obs + (size_t)env * kFrameBytes, kFrameBytes, lane);
     }
@@ -416,8 +445,8 @@ __global__ void __launch_bounds__(128) step_kernel(Params p) {
 __global__ void __launch_bounds__(128) debug_kernel(Params p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const Ctx c = stage_block(p, smem, false);
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < p.N;
+  uint32_t i = 0;
+  const bool active = env_of_thread(p, i);
   const size_t N = p.N;
   uint4* st = reinterpret_cast<uint4*>(p.state);
   Cpu m{};
@@ -471,7 +500,7 @@ __global__ void __launch_bounds__(128) cache_kernel(Params p) {
     const uint32_t lo = m.rd<false>(c, 0x1FFCu), hi = m.rd<false>(c, 0x1FFDu);
     m.PC = lo | (hi << 8);
     set_inputs(m, 0);
-    frame_out = kGray ? p.cache_staging + (size_t)j * kFrameBytes : p.cache_obs_out + (size_t)j * kFrameBytes;
+    frame_out = kGray ? p.cache_staging + (size_t)j * (2 * kFrameBytes) : p.cache_obs_out + (size_t)j * kFrameBytes;
     if (nframes == 0)
       for (uint32_t q = 0; q < (uint32_t)kFrameChunks; ++q) reinterpret_cast<uint4*>(frame_out)[q] = make_uint4(0, 0, 0, 0);
   }
@@ -499,7 +528,11 @@ __global__ void __launch_bounds__(128) cache_kernel(Params p) {
       const uint32_t zf = __shfl_sync(kFull, zero_obs, l);
       uint8_t* o = p.cache_obs_out + (size_t)ent * kObs84;
       if (zf) warp_zero(o, kObs84, lane);
-      else warp_area84(p.cache_staging + (size_t)ent * kFrameBytes, o, lane);
+      else {
+        const uint8_t* pair = p.cache_staging + (size_t)ent * (2 * kFrameBytes);
+        const uint32_t nf = __shfl_sync(kFull, nframes, l);
+        warp_area84(pair + kFrameBytes, nf >= 2 ? pair : nullptr, o, lane);
+      }
     }
   }
 }

@@ -55,43 +55,37 @@ __device__ __forceinline__ uint32_t nib_bytes(uint32_t n) {  // nibble -> 0x00/0
 }
 
 // ---- pixel writer (state in shared memory between flushes) --------------------------------
+// fill whole chunks [c0, c1) with one 4-byte pattern (frame start/end only: out of line)
+__device__ __noinline__ void fill_chunks(uint8_t* base, int32_t c0, int32_t c1, uint32_t fill) {
+  uint4* p = reinterpret_cast<uint4*>(base);
+  for (int32_t k = c0; k < c1; ++k) p[k] = make_uint4(fill, fill, fill, fill);
+}
+
 struct PixWriter {
   uint8_t* base;
-  int32_t chunk;
+  int32_t chunk;  // chunk being assembled (-1: none yet)
   uint32_t w0, w1, w2, w3, fill;
-  bool max_mode;
 
-  __device__ __forceinline__ void store_chunk(int32_t c, uint32_t a, uint32_t b, uint32_t d, uint32_t e) {
-    uint4* p = reinterpret_cast<uint4*>(base) + c;
-    if (max_mode) {
-      uint4 o = *p;
-      a = __vmaxu4(a, o.x); b = __vmaxu4(b, o.y); d = __vmaxu4(d, o.z); e = __vmaxu4(e, o.w);
-    }
-    *p = make_uint4(a, b, d, e);
-  }
   __device__ __forceinline__ void advance_to(int32_t c) {
-    if (chunk >= 0) store_chunk(chunk, w0, w1, w2, w3);
-    if (!(max_mode && fill == 0))
-      for (int32_t k = chunk + 1; k < c; ++k) store_chunk(k, fill, fill, fill, fill);
+    if (chunk >= 0) reinterpret_cast<uint4*>(base)[chunk] = make_uint4(w0, w1, w2, w3);
+    if (c > chunk + 1) fill_chunks(base, chunk + 1, c, fill);
     chunk = c;
     w0 = w1 = w2 = w3 = fill;
   }
-  __device__ __forceinline__ void put(int32_t g, uint32_t px, uint32_t bmask) {
-    int32_t c = g >> 2;
+  // merge the masked bytes of one 16-pixel chunk (pixels arrive in raster order)
+  __device__ __forceinline__ void emit(int32_t c, uint32_t p0, uint32_t p1, uint32_t p2, uint32_t p3,
+                                       uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
     if (c != chunk) advance_to(c);
-    switch (g & 3) {
-      case 0: w0 = (w0 & ~bmask) | (px & bmask); break;
-      case 1: w1 = (w1 & ~bmask) | (px & bmask); break;
-      case 2: w2 = (w2 & ~bmask) | (px & bmask); break;
-      default: w3 = (w3 & ~bmask) | (px & bmask); break;
-    }
+    w0 = (w0 & ~m0) | (p0 & m0);
+    w1 = (w1 & ~m1) | (p1 & m1);
+    w2 = (w2 & ~m2) | (p2 & m2);
+    w3 = (w3 & ~m3) | (p3 & m3);
   }
   __device__ __forceinline__ void load(const uint32_t* w, uint32_t s) {
     base = reinterpret_cast<uint8_t*>((uint64_t)w[0] | ((uint64_t)w[s] << 32));
     chunk = (int32_t)w[2 * s];
     w0 = w[3 * s]; w1 = w[4 * s]; w2 = w[5 * s]; w3 = w[6 * s];
     fill = w[7 * s];
-    max_mode = (w[8 * s] & 2u) != 0;
   }
   __device__ __forceinline__ void save(uint32_t* w, uint32_t s) const {
     w[2 * s] = (uint32_t)chunk;
@@ -99,14 +93,21 @@ struct PixWriter {
   }
 };
 
-// begin rendering a frame: writer state in shared memory (flags bit0 = render, bit1 = max)
-__device__ __forceinline__ void pw_begin(uint32_t* w, uint32_t s, uint8_t* base, uint32_t fill4, bool mx) {
+// byte mask of the pixels of group [xg, xg+4) that lie in [xa, xb)
+__device__ __forceinline__ uint32_t group_mask(uint32_t xg, uint32_t xa, uint32_t xb) {
+  if (xb <= xg || xa >= xg + 4u) return 0u;
+  const uint32_t lo = xa > xg ? xa - xg : 0u, hi = xb < xg + 4u ? xb - xg : 4u;
+  return (0xFFFFFFFFu >> (32u - 8u * (hi - lo))) << (8u * lo);
+}
+
+// begin rendering a frame: writer state in shared memory (flags bit0 = render)
+__device__ __forceinline__ void pw_begin(uint32_t* w, uint32_t s, uint8_t* base, uint32_t fill4) {
   const uint64_t b = reinterpret_cast<uint64_t>(base);
   w[0] = (uint32_t)b; w[s] = (uint32_t)(b >> 32);
   w[2 * s] = 0xFFFFFFFFu;  // chunk -1
   w[3 * s] = w[4 * s] = w[5 * s] = w[6 * s] = fill4;
   w[7 * s] = fill4;
-  w[8 * s] = 1u | (mx ? 2u : 0u);
+  w[8 * s] = 1u;
 }
 __device__ __forceinline__ bool pw_rendering(const uint32_t* w, uint32_t s) { return (w[8 * s] & 1u) != 0; }
 __device__ __forceinline__ void pw_end(uint32_t* w, uint32_t s) {
@@ -156,61 +157,68 @@ struct Tia {
     w[8 * s] = t_tia;
   }
 
-  struct Masks { uint32_t p0[5], p1[5], m0[5], m1[5], bl[5], pf[5]; };
-
-  __device__ __forceinline__ static void place(uint32_t* m, uint32_t pat, uint32_t p) {
-    uint32_t wi = p >> 5, s = p & 31;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      if (k == (int)wi) m[k] |= pat << s;
-      if (s && k == (int)(wi == 4 ? 0 : wi + 1)) m[k] |= pat >> (32 - s);
+  // a 160-pixel line as five named 32-bit words (no arrays: everything stays in registers)
+  struct W5 {
+    uint32_t a, b, c, d, e;
+    __device__ __forceinline__ uint32_t operator[](int k) const {
+      return k == 0 ? a : k == 1 ? b : k == 2 ? c : k == 3 ? d : e;
     }
-  }
+    __device__ __forceinline__ void zero() { a = b = c = d = e = 0u; }
+    // OR a <=32-bit pattern starting at pixel p (0..159) into the circular line
+    __device__ __forceinline__ void place(uint32_t pat, uint32_t p) {
+      const uint32_t wi = p >> 5, s = p & 31u;
+      const uint32_t lo = pat << s, hi = s ? (pat >> (32u - s)) : 0u;
+      a |= (wi == 0 ? lo : 0u) | (wi == 4 ? hi : 0u);
+      b |= (wi == 1 ? lo : 0u) | (wi == 0 ? hi : 0u);
+      c |= (wi == 2 ? lo : 0u) | (wi == 1 ? hi : 0u);
+      d |= (wi == 3 ? lo : 0u) | (wi == 2 ? hi : 0u);
+      e |= (wi == 4 ? lo : 0u) | (wi == 3 ? hi : 0u);
+    }
+  };
+  struct Masks { W5 p0, p1, m0, m1, bl, pf; };
+
   // NUSIZ copy set: bit0 +0, bit1 +16, bit2 +32, bit3 +64
   __device__ __forceinline__ static uint32_t copies(uint32_t mode) { return (0x1D197531u >> (4 * mode)) & 0xF; }
-  __device__ __forceinline__ static void player_mask(uint32_t* m, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) m[k] = 0;
-    if (g == 0) return;
-    uint32_t mode = nusiz & 7;
-    uint32_t pat = refl ? g : rev8(g);
-    if (mode == 5) pat = spread2(pat);
-    else if (mode == 7) pat = spread4(pat);
-    uint32_t cp = copies(mode);
+  __device__ __forceinline__ static void place_copies(W5& m, uint32_t pat, uint32_t pos, uint32_t cp) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
       if (cp & (1u << c)) {
-        uint32_t p = pos + (c == 0 ? 0u : (8u << c));
-        place(m, pat, p >= 160u ? p - 160u : p);
+        const uint32_t p = pos + (c == 0 ? 0u : (8u << c));
+        m.place(pat, p >= 160u ? p - 160u : p);
       }
   }
-  __device__ __forceinline__ static void missile_mask(uint32_t* m, uint32_t pos, uint32_t nusiz, bool en) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) m[k] = 0;
+  __device__ __forceinline__ static void player_mask(W5& m, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl) {
+    m.zero();
+    if (g == 0) return;
+    const uint32_t mode = nusiz & 7;
+    uint32_t pat = refl ? g : rev8(g);  // pixel d shows graphic bit 7-d (bit d when reflected)
+    if (mode == 5) pat = spread2(pat);
+    else if (mode == 7) pat = spread4(pat);
+    place_copies(m, pat, pos, copies(mode));
+  }
+  __device__ __forceinline__ static void missile_mask(W5& m, uint32_t pos, uint32_t nusiz, bool en) {
+    m.zero();
     if (!en) return;
-    uint32_t mode = nusiz & 7;
-    uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3))) - 1u;
-    uint32_t cp = (mode == 5 || mode == 7) ? 1u : copies(mode);
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (cp & (1u << c)) {
-        uint32_t p = pos + (c == 0 ? 0u : (8u << c));
-        place(m, pat, p >= 160u ? p - 160u : p);
-      }
+    const uint32_t mode = nusiz & 7;
+    const uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3))) - 1u;
+    place_copies(m, pat, pos, (mode == 5 || mode == 7) ? 1u : copies(mode));
   }
   __device__ __forceinline__ void build_masks(Masks& M) const {
     player_mask(M.p0, posP0, nusiz0, f(7) ? grp0o : grp0n, f(1));
     player_mask(M.p1, posP1, nusiz1, f(8) ? grp1o : grp1n, f(2));
     missile_mask(M.m0, posM0, nusiz0, f(3) && !f(10));
     missile_mask(M.m1, posM1, nusiz1, f(4) && !f(11));
-#pragma unroll
-    for (int k = 0; k < 5; ++k) M.bl[k] = 0;
-    if (f(9) ? f(6) : f(5)) place(M.bl, (1u << (1u << ((ctrlpf >> 4) & 3))) - 1u, posBL);
-    uint32_t left = ((pf0 >> 4) & 0xF) | (rev8(pf1) << 4) | ((pf2 & 0xFF) << 12);
-    uint32_t right = (ctrlpf & 1) ? (__brev(left) >> 12) : left;
-    uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
-#pragma unroll
-    for (int k = 0; k < 5; ++k) M.pf[k] = spread4((uint32_t)(cells >> (8 * k)));
+    M.bl.zero();
+    if (f(9) ? f(6) : f(5)) M.bl.place((1u << (1u << ((ctrlpf >> 4) & 3))) - 1u, posBL);
+    // playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), each 4 pixels wide
+    const uint32_t left = ((pf0 >> 4) & 0xF) | (rev8(pf1) << 4) | ((pf2 & 0xFF) << 12);
+    const uint32_t right = (ctrlpf & 1) ? (__brev(left) >> 12) : left;
+    const uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
+    M.pf.a = spread4((uint32_t)cells);
+    M.pf.b = spread4((uint32_t)(cells >> 8));
+    M.pf.c = spread4((uint32_t)(cells >> 16));
+    M.pf.d = spread4((uint32_t)(cells >> 24));
+    M.pf.e = spread4((uint32_t)(cells >> 32));
   }
 
   // OR the collision latches of visible pixels [xa, xb) (bit 2r = d7, 2r+1 = d6 of register r)
@@ -240,46 +248,53 @@ struct Tia {
     return (gray ? (uint32_t)gray[idx] : idx) * 0x01010101u;
   }
 
+  // 4 pixels of group g (x = 4g..4g+3) from the four class masks of its 32-pixel word
+  __device__ __forceinline__ static uint32_t group_px(uint32_t q0, uint32_t q1, uint32_t qb, uint32_t qp,
+                                                     uint32_t sh, bool pfp, uint32_t c0, uint32_t c1,
+                                                     uint32_t cbl, uint32_t cp, uint32_t cbk) {
+    const uint32_t np0 = (q0 >> sh) & 0xF, np1 = (q1 >> sh) & 0xF, nbl = (qb >> sh) & 0xF, npf = (qp >> sh) & 0xF;
+    uint32_t e0, e1, eb, ep;
+    if (!pfp) {
+      e0 = np0; e1 = np1 & ~e0; eb = nbl & ~(e0 | e1); ep = npf & ~(e0 | e1 | nbl);
+    } else {
+      eb = nbl; ep = npf & ~nbl; e0 = np0 & ~(nbl | npf); e1 = np1 & ~(nbl | npf | np0);
+    }
+    const uint32_t B0 = nib_bytes(e0), B1 = nib_bytes(e1), Bb = nib_bytes(eb), Bp = nib_bytes(ep);
+    return (c0 & B0) | (c1 & B1) | (cbl & Bb) | (cp & Bp) | (cbk & ~(B0 | B1 | Bb | Bp));
+  }
+
+  // pixels [xa, xb) of window row `row`, one 16-pixel chunk (4 groups) per iteration
   __device__ __forceinline__ void render_span(const Masks& M, PixWriter& pw, uint32_t line, uint32_t row,
                                               uint32_t xa, uint32_t xb, const uint8_t* gray) {
-    uint32_t cbk = shade(colubk, gray), c0 = shade(colup0, gray), c1 = shade(colup1, gray),
-             cbl = shade(colupf, gray);
-    uint32_t cpl = (ctrlpf & 2) ? c0 : cbl, cpr = (ctrlpf & 2) ? c1 : cbl;
-    bool pfp = ctrlpf & 4;
-    bool comb = (int32_t)line == comb_line;
-    uint32_t base_g = row * (kFrameW / 4);
-    for (uint32_t g = xa >> 2; g <= (xb - 1) >> 2; ++g) {
-      uint32_t k = g >> 3, sh = (g & 7) * 4;
-      uint32_t q0 = 0, q1 = 0, qb = 0, qp = 0;
+    const uint32_t cbk = shade(colubk, gray), c0 = shade(colup0, gray), c1 = shade(colup1, gray),
+                   cbl = shade(colupf, gray);
+    const uint32_t cpl = (ctrlpf & 2) ? c0 : cbl, cpr = (ctrlpf & 2) ? c1 : cbl;
+    const bool pfp = ctrlpf & 4;
+    const bool comb = (int32_t)line == comb_line;
+    for (uint32_t c = xa >> 4; c <= (xb - 1) >> 4; ++c) {
+      const int k = (int)(c >> 1);
+      const uint32_t hs = 16u * (c & 1u);
+      const uint32_t q0 = (M.p0[k] | M.m0[k]) >> hs, q1 = (M.p1[k] | M.m1[k]) >> hs;
+      const uint32_t qb = M.bl[k] >> hs, qp = M.pf[k] >> hs;
+      const uint32_t x0 = 16u * c;
+      const uint32_t cp = x0 < 80u ? cpl : cpr;
+      const bool pf_only = ((q0 | q1 | qb) & 0xFFFFu) == 0;
+      uint32_t px[4], bm[4];
 #pragma unroll
-      for (int kk = 0; kk < 5; ++kk)
-        if (kk == (int)k) {
-          q0 = M.p0[kk] | M.m0[kk]; q1 = M.p1[kk] | M.m1[kk]; qb = M.bl[kk]; qp = M.pf[kk];
-        }
-      uint32_t np0 = (q0 >> sh) & 0xF, np1 = (q1 >> sh) & 0xF, nbl = (qb >> sh) & 0xF, npf = (qp >> sh) & 0xF;
-      uint32_t e0, e1, eb, ep;
-      if (!pfp) {
-        e0 = np0; e1 = np1 & ~e0; eb = nbl & ~(e0 | e1); ep = npf & ~(e0 | e1 | nbl);
-      } else {
-        eb = nbl; ep = npf & ~nbl; e0 = np0 & ~(nbl | npf); e1 = np1 & ~(nbl | npf | np0);
+      for (int j = 0; j < 4; ++j) {
+        px[j] = pf_only ? (cbk ^ ((cbk ^ cp) & nib_bytes(qp >> (4 * j))))
+                        : group_px(q0, q1, qb, qp, 4u * j, pfp, c0, c1, cbl, cp, cbk);
+        bm[j] = group_mask(x0 + 4u * j, xa, xb);
       }
-      uint32_t B0 = nib_bytes(e0), B1 = nib_bytes(e1), Bb = nib_bytes(eb), Bp = nib_bytes(ep);
-      uint32_t cp = g < 20 ? cpl : cpr;
-      uint32_t px = (c0 & B0) | (c1 & B1) | (cbl & Bb) | (cp & Bp) | (cbk & ~(B0 | B1 | Bb | Bp));
-      if (comb && g < 2) px = pw.fill;
-      uint32_t x0 = g * 4;
-      uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 4 ? xb - x0 : 4u;
-      uint32_t bm = (0xFFFFFFFFu >> (32 - 8 * (hi - lo))) << (8 * lo);
-      pw.put((int32_t)(base_g + g), px, bm);
+      if (comb && c == 0) { px[0] = pw.fill; px[1] = pw.fill; }  // HMOVE comb, x < 8 (R#11)
+      pw.emit((int32_t)(row * 10u + c), px[0], px[1], px[2], px[3], bm[0], bm[1], bm[2], bm[3]);
     }
   }
   __device__ __forceinline__ static void render_black(PixWriter& pw, uint32_t row, uint32_t xa, uint32_t xb) {
-    uint32_t base_g = row * (kFrameW / 4);
-    for (uint32_t g = xa >> 2; g <= (xb - 1) >> 2; ++g) {
-      uint32_t x0 = g * 4;
-      uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 4 ? xb - x0 : 4u;
-      uint32_t bm = (0xFFFFFFFFu >> (32 - 8 * (hi - lo))) << (8 * lo);
-      pw.put((int32_t)(base_g + g), pw.fill, bm);
+    for (uint32_t c = xa >> 4; c <= (xb - 1) >> 4; ++c) {
+      const uint32_t x0 = 16u * c;
+      pw.emit((int32_t)(row * 10u + c), pw.fill, pw.fill, pw.fill, pw.fill, group_mask(x0, xa, xb),
+              group_mask(x0 + 4u, xa, xb), group_mask(x0 + 8u, xa, xb), group_mask(x0 + 12u, xa, xb));
     }
   }
 

@@ -84,6 +84,17 @@ def test_mixed_roms_ragged():
     run_parity(gpu, ref, 30, check_every=10)
 
 
+@pytest.mark.parametrize("epw", ["1", "4", "32"])
+def test_launch_shape_independence(epw, monkeypatch):
+    """Results do not depend on the launch shape: envs per warp (CULE_EPW), block size and
+    the ROM-grouped env-to-lane permutation (S:283-286 worker-count independence)."""
+    monkeypatch.setenv("CULE_EPW", epw)
+    monkeypatch.setenv("CULE_BLOCK", "64")
+    roms = [games.build_rom(n) for n in ("R1", "R3", "R2")]
+    gpu, ref = pair(roms, 77, 4, reset_cache_size=4, env_index_base=5)
+    run_parity(gpu, ref, 12, check_every=4)
+
+
 def test_raw_fs4_and_fs2():
     gpu, ref = pair([games.build_rom("R2")], 40, 4, "raw", reset_cache_size=4)
     run_parity(gpu, ref, 20, check_every=4)
