@@ -33,9 +33,15 @@ CONFIGS = {
     "cfg4": (["R1", "R2", "R3", "R4"], 32768, 4, "gray84", "cfg4: 32768 envs, R1-R4 interleaved, fs=4, GRAY84"),
 }
 
-# SASS thread-instructions the step kernel executes per raw frame on cfg2 (measured with
-# ncu smsp__thread_inst_executed.sum; profiles/ holds the capture).  Used for the issue roof.
-INST_PER_FRAME = {"cfg2": None, "cfg3": None, "cfg4": None}
+# The step kernel is bound by instruction issue: per raw frame it issues a
+# fixed number of warp-instructions, measured once per build with ncu (smsp__inst_executed.sum
+# / frames per launch) and committed under profiles/.  achieved = that x frames per launch /
+# the live launch time; peak = 148 SMs x 4 schedulers x 1 warp-instruction/cycle x max clock.
+# DRAM traffic per launch comes from the same capture.
+ISSUE_PROFILE = {
+    "cfg2": {"warp_inst_per_frame": 577100.0, "dram_bytes_per_launch": 546.4e6,
+             "source": "profiles/r01_v3_step_kernel_ncu.txt"},
+}
 
 
 def parse():
@@ -202,6 +208,7 @@ def run_cule(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_1907_08467_b200 import Env, build
+    from paper_1907_08467_b200 import dist as D
     from paper_1907_08467_b200.inputs import games
 
     build.build()
@@ -211,7 +218,8 @@ def run_cule(args, rank, world, local_rank):
     if args.envs:
         envs = args.envs
     roms = [games.build_rom(n) for n in rom_names]
-    env = Env(roms, envs, fs, obs_mode=mode, env_index_base=rank * envs, device=dev)
+    base, _ = D.shard(envs, rank)
+    env = Env(roms, envs, fs, obs_mode=mode, env_index_base=base, device=dev)
     stream = torch.cuda.current_stream(dev)
     env.reset(0)
     gen = torch.Generator(device=dev)
@@ -239,12 +247,8 @@ def run_cule(args, rank, world, local_rank):
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    counters = env.counters().clone()
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
-    ms_max = float(ms_t.item())
+    ms_max = D.max_over_ranks(ms, device=dev)
+    counters = D.reduce_counters(env.counters())
     frames_total = envs * world * fs * K
     fps = frames_total / (ms_max / 1000.0)
 
@@ -266,11 +270,8 @@ def run_cule(args, rank, world, local_rank):
     for t in range(args.e2e_steps):
         h_act.copy_(host_acts[t])
         env.step_host(h_act, h_obs, h_rew, h_done)
-    e_dt = time.perf_counter() - e0
-    e_t = torch.tensor([e_dt], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-    e2e_fps = envs * world * fs * args.e2e_steps / float(e_t.item())
+    e_dt = D.max_over_ranks(time.perf_counter() - e0, device=dev)
+    e2e_fps = envs * world * fs * args.e2e_steps / e_dt
 
     if rank != 0:
         return
@@ -281,11 +282,13 @@ def run_cule(args, rank, world, local_rank):
     alg_bytes = alg_bytes_per_env * envs
     hbm_gbs = alg_bytes / launch_s / 1e9
     sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
-    issue_peak = 148 * 4 * 32 * pk["sm_max_mhz"] * 1e6 / 1e12  # T lane-instr/s at max clock
-    ipf = INST_PER_FRAME.get(args.config)
-    roof = {"bound": "alu", "unit": "Tinst/s", "peak": issue_peak,
+    issue_peak = 148 * 4 * pk["sm_max_mhz"] * 1e6 / 1e12  # T warp-instr/s at max clock
+    prof = ISSUE_PROFILE.get(args.config) if not args.envs else None
+    ipf = prof["warp_inst_per_frame"] if prof else None
+    roof = {"bound": "alu", "unit": "Twarp-inst/s", "peak": issue_peak,
             "achieved": (ipf * envs * fs / launch_s / 1e12) if ipf else None,
-            "traffic": None,
+            "traffic": prof["dram_bytes_per_launch"] if prof else None,
+            "profile": prof["source"] if prof else None,
             "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk["hbm_gbs"], "frac": hbm_gbs / pk["hbm_gbs"],
                     "alg_bytes_per_launch": alg_bytes},
             "peak_source": pk["source"]}
