@@ -284,7 +284,7 @@ struct Tia {
       for (int j = 0; j < 4; ++j) {
         px[j] = pf_only ? (cbk ^ ((cbk ^ cp) & nib_bytes(qp >> (4 * j))))
                         : group_px(q0, q1, qb, qp, 4u * j, pfp, c0, c1, cbl, cp, cbk);
-        bm[j] = group_mask(x0 + 4u * j, xa, xb);
+        bm[j] = (xa <= x0 && xb >= x0 + 16u) ? 0xFFFFFFFFu : group_mask(x0 + 4u * j, xa, xb);
       }
       if (comb && c == 0) { px[0] = pw.fill; px[1] = pw.fill; }  // HMOVE comb, x < 8 (R#11)
       pw.emit((int32_t)(row * 10u + c), px[0], px[1], px[2], px[3], bm[0], bm[1], bm[2], bm[3]);
@@ -298,30 +298,56 @@ struct Tia {
     }
   }
 
-  // advance over colour clocks [t_tia, t_to)
+  // collision latches the objects present now could still set (an absent object cannot
+  // collide); when they are all set already, a span needs no collision work at all
+  __device__ __forceinline__ uint32_t open_pairs() const {
+    const uint32_t p0 = (f(7) ? grp0o : grp0n) != 0u, p1 = (f(8) ? grp1o : grp1n) != 0u;
+    const uint32_t m0 = f(3) & (f(10) ^ 1u), m1 = f(4) & (f(11) ^ 1u);
+    const uint32_t bl = f(9) ? f(6) : f(5);
+    const uint32_t pf = ((pf0 & 0xF0u) | pf1 | pf2) != 0u;
+    const uint32_t possible = (m0 & p1) | ((m0 & p0) << 1) | ((m1 & p0) << 2) | ((m1 & p1) << 3) |
+                              ((p0 & pf) << 4) | ((p0 & bl) << 5) | ((p1 & pf) << 6) | ((p1 & bl) << 7) |
+                              ((m0 & pf) << 8) | ((m0 & bl) << 9) | ((m1 & pf) << 10) | ((m1 & bl) << 11) |
+                              ((bl & pf) << 12) | ((p0 & p1) << 14) | ((m0 & m1) << 15);
+    return possible & ~coll;
+  }
+
+  // advance over colour clocks [t_tia, t_to) with the current register values
   __device__ __forceinline__ void catch_up(uint32_t t_to, bool render, PixWriter& pw, uint32_t ystart,
                                            const uint8_t* gray) {
-    uint32_t t0 = t_tia;
+    const uint32_t t0 = t_tia;
     if (t_to <= t0) return;
     t_tia = t_to;
-    uint32_t l0 = t0 / 228u, l1 = (t_to - 1) / 228u;
-    bool have = false, full_done = false;
+    const uint32_t l0 = t0 / 228u, l1 = (t_to - 1) / 228u;
+    // visible x range of the first and last line ([xa0,160) on l0, [0,xb1) on l1)
+    const uint32_t h0 = t0 - l0 * 228u, h1 = t_to - l1 * 228u;
+    const uint32_t xa0 = h0 > 68u ? h0 - 68u : 0u;
+    const uint32_t xb1 = h1 > 68u ? h1 - 68u : 0u;
+    const bool vblank = f(0) != 0u;
+    const bool need_coll = !vblank && open_pairs() != 0u;
+    const uint32_t w0 = ystart, w1 = ystart + (uint32_t)kFrameH;  // window lines [w0, w1)
+    const bool any_win = render && l1 >= w0 && l0 < w1;
+    if (!need_coll && !any_win) return;
     Masks M;
-    for (uint32_t ln = l0; ln <= l1; ++ln) {
-      uint32_t h0 = (ln == l0) ? t0 - ln * 228u : 0u;
-      uint32_t h1 = (ln == l1) ? t_to - ln * 228u : 228u;
-      if (h1 <= 68u) continue;
-      uint32_t xa = h0 > 68u ? h0 - 68u : 0u, xb = h1 - 68u;
-      bool inwin = render && ln >= ystart && ln < ystart + (uint32_t)kFrameH;
-      if (f(0)) {  // VBLANK: black, no collisions
-        if (inwin) render_black(pw, ln - ystart, xa, xb);
-        continue;
+    if (!vblank) build_masks(M);
+    if (need_coll) {
+      // collisions depend on x only: the union of the span's visible x ranges suffices
+      if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) {
+        collide(M, 0u, 160u);
+      } else if (l1 == l0) {
+        if (xb1 > xa0) collide(M, xa0, xb1);
+      } else {
+        if (xa0 < 160u) collide(M, xa0, 160u);
+        if (xb1 > 0u) collide(M, 0u, xb1);
       }
-      if (!have) { build_masks(M); have = true; }
-      bool full = xa == 0 && xb == 160u;
-      if (!(full && full_done)) collide(M, xa, xb);
-      if (full) full_done = true;
-      if (inwin) render_span(M, pw, ln, ln - ystart, xa, xb, gray);
+    }
+    if (!any_win) return;
+    const uint32_t la = l0 > w0 ? l0 : w0, lb = l1 < w1 - 1u ? l1 : w1 - 1u;
+    for (uint32_t ln = la; ln <= lb; ++ln) {
+      const uint32_t xa = ln == l0 ? xa0 : 0u, xb = ln == l1 ? xb1 : 160u;
+      if (xb <= xa) continue;
+      if (vblank) render_black(pw, ln - ystart, xa, xb);
+      else render_span(M, pw, ln, ln - ystart, xa, xb, gray);
     }
   }
 
