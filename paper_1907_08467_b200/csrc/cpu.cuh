@@ -150,109 +150,97 @@ struct Cpu {
     } else {
       op = rd<true>(c, pc);
       d = c.decode[op];
-      const uint32_t len = (uint32_t)(d >> dk::LEN) & 3u;
+      const uint32_t len = (uint32_t)d & 3u;
       b1 = len > 1 ? rd<true>(c, pc + 1) : 0u;
       b2 = len > 2 ? rd<true>(c, pc + 2) : 0u;
     }
-    const uint32_t lo32 = (uint32_t)d, hi32 = (uint32_t)(d >> 32);
-    const uint32_t spc = (hi32 >> (dk::SPC - 32)) & 0xFu;
+    const uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
+    const uint32_t spc = (hi >> dk::SPC) & 0xFu;
     if (spc == SP_JAM) { PC = (pc + 1) & 0xFFFFu; fault = 1; return EV_FAULT; }
-    const uint32_t mode = lo32 & 0xFu;
-    uint32_t n = (lo32 >> dk::CYC) & 0xFu;
-    PC = (pc + ((lo32 >> dk::LEN) & 3u)) & 0xFFFFu;
+    uint32_t n = (lo >> dk::CYC) & 0xFu;
+    PC = (pc + (lo & 3u)) & 0xFFFFu;
 
-    // ---- phase A: effective address (all modes computed arithmetically) ----------------------
-    const uint32_t zidx = (mode == AM_ZPX || mode == AM_INDX) ? X : (mode == AM_ZPY ? Y : 0u);
-    const uint32_t zpa = (b1 + zidx) & 0xFFu;
+    // ---- phase A: effective address --------------------------------------------------------------
+    const uint32_t zpa = (b1 + ((lo & dk::ZIX) ? X : 0u) + ((lo & dk::ZIY) ? Y : 0u)) & 0xFFu;
     uint32_t base = b1 | (b2 << 8);
-    if (mode == AM_INDX || mode == AM_INDY || mode == AM_IND) {
-      const uint32_t p0 = mode == AM_IND ? base : zpa;
-      const uint32_t p1 = mode == AM_IND ? ((base & 0xFF00u) | ((base + 1) & 0xFFu)) : ((zpa + 1) & 0xFFu);
+    if (lo & (dk::PTRZ | dk::PTRA)) {
+      const bool pa = (lo & dk::PTRA) != 0;
+      const uint32_t p0 = pa ? base : zpa;
+      const uint32_t p1 = pa ? ((base & 0xFF00u) | ((base + 1) & 0xFFu)) : ((zpa + 1) & 0xFFu);
       const uint32_t plo = rd<true>(c, p0);
       const uint32_t phi = rd<true>(c, p1);
       base = plo | (phi << 8);
     }
-    const uint32_t aidx = mode == AM_ABSX ? X : ((mode == AM_ABSY || mode == AM_INDY) ? Y : 0u);
-    const uint32_t ea16 = (base + aidx) & 0xFFFFu;
-    const bool zpmode = mode == AM_ZP || mode == AM_ZPX || mode == AM_ZPY;
-    const uint32_t ea = zpmode ? zpa : ea16;
-    n += ((lo32 >> dk::PEN) & 1u) & (((ea16 ^ base) >> 8) & 1u);
-    if ((hi32 >> (dk::BR - 32)) & 1u) {
-      const uint32_t sel = (hi32 >> (dk::BRF - 32)) & 3u;
-      const uint32_t flag = sel == 0 ? (nreg >> 7) & 1u : sel == 1 ? V : sel == 2 ? C : ((zreg & 0xFFu) == 0 ? 1u : 0u);
-      if (flag == ((hi32 >> (dk::BRT - 32)) & 1u)) {
-        const uint32_t tgt = (PC + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
-        n += 1u + (((tgt ^ PC) >> 8) & 1u);
-        PC = tgt;
-      }
+    const uint32_t ea16 = (base + ((lo & dk::AIX) ? X : 0u) + ((lo & dk::AIY) ? Y : 0u)) & 0xFFFFu;
+    const uint32_t ea = (lo & dk::ZP) ? zpa : ea16;
+    if ((lo & dk::PEN) && ((ea16 ^ base) & 0x100u)) ++n;
+    if (lo & dk::BR) {
+      const uint32_t flags4 = ((nreg >> 7) & 1u) | (V << 1) | (C << 2) | ((zreg & 0xFFu) == 0 ? 8u : 0u);
+      const uint32_t taken = ((flags4 >> ((hi >> dk::BRF) & 3u)) ^ ((hi & dk::BRT) ? 0u : 1u)) & 1u;
+      const uint32_t tgt = (PC + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
+      n += taken ? 1u + (((tgt ^ PC) >> 8) & 1u) : 0u;
+      PC = taken ? tgt : PC;
     }
-    if ((hi32 >> (dk::JMP - 32)) & 1u) PC = ea;
+    if (lo & dk::JMP) PC = ea;
 
-    // ---- phase C ------------------------------------------------------------------------------
+    // ---- phase C ---------------------------------------------------------------------------------
     now = fc + n;
     uint32_t v = b1;  // immediate operand
-    if ((lo32 >> dk::RD) & 1u) v = rd<false>(c, ea);
+    if (lo & dk::RD) v = rd<false>(c, ea);
 
     if (spc) {
       special(c, spc, v, ea);
     } else {
-      const uint32_t rsrc = (lo32 >> dk::RSRC) & 3u;
-      const uint32_t R = rsrc == RG_A ? A : rsrc == RG_X ? X : rsrc == RG_Y ? Y : SP;
-      const uint32_t M = ((lo32 >> dk::OPR) & 1u) ? R : v;
-      const uint32_t u1 = (lo32 >> dk::U1) & 7u, u2 = (lo32 >> dk::U2) & 7u;
-      // unit1: shifts / rotates / inc / dec
-      const bool sl = u1 == U1_ASL || u1 == U1_ROL, sr = u1 == U1_LSR || u1 == U1_ROR;
-      const uint32_t shl = ((M << 1) | (u1 == U1_ROL ? C : 0u)) & 0xFFu;
-      const uint32_t shr = (M >> 1) | (u1 == U1_ROR ? (C << 7) : 0u);
-      const uint32_t idc = (M + (u1 == U1_INC ? 1u : (u1 == U1_DEC ? 0xFFu : 0u))) & 0xFFu;
-      const uint32_t r1 = sl ? shl : (sr ? shr : idc);
-      const uint32_t c1 = sl ? (M >> 7) : (sr ? (M & 1u) : C);
-      // unit2: logic / adder (ADC, SBC, CMP share it) / BIT
-      const bool cmp = u2 == U2_CMP, sub = u2 == U2_SBC || cmp, arith = u2 >= U2_ADC && u2 <= U2_CMP;
-      const uint32_t lhs = cmp ? R : A;
-      const uint32_t add = sub ? (r1 ^ 0xFFu) : r1;
-      const uint32_t sum = lhs + add + (cmp ? 1u : c1);
-      const uint32_t rlog = u2 == U2_OR ? (A | r1) : (u2 == U2_AND ? (A & r1) : (A ^ r1));
-      uint32_t r2 = u2 == U2_PASS ? r1 : (arith ? (sum & 0xFFu) : rlog);
-      uint32_t nC = arith ? (sum >> 8) : c1;
-      uint32_t nV = (u2 == U2_ADC || u2 == U2_SBC) ? ((~(lhs ^ add) & (lhs ^ sum)) >> 7) & 1u
-                  : (u2 == U2_BIT ? (r1 >> 6) & 1u : V);
-      uint32_t nn = u2 == U2_BIT ? r1 : r2, nz_ = u2 == U2_BIT ? (A & r1) : r2;
-      if (D && (u2 == U2_ADC || u2 == U2_SBC)) decimal(u2, r1, c1, r2, nC, nV, nn, nz_);
-      if ((lo32 >> dk::WR) & 1u) {
-        const uint32_t sv = ((lo32 >> dk::SAX) & 1u) ? (A & X) : R;
-        wr(c, ea, ((lo32 >> dk::WSEL) & 1u) ? sv : r1);
-      }
-      const uint32_t dst = (lo32 >> dk::DST) & 7u;
-      if (dst == DS_A || dst == DS_AX) A = r2;
-      if (dst == DS_X || dst == DS_AX) X = r2;
-      if (dst == DS_Y) Y = r2;
-      if (dst == DS_SP) SP = r2;
-      if ((lo32 >> dk::NZ) & 1u) { nreg = nn; zreg = nz_ & 0xFFu; }
+      // register operand and unit1 (shift / rotate / increment)
+      const uint32_t R = ((lo & dk::RA) ? A : 0u) | ((lo & dk::RX) ? X : 0u) | ((lo & dk::RY) ? Y : 0u) |
+                         ((lo & dk::RS) ? SP : 0u);
+      const uint32_t M = (lo & dk::OPR) ? R : v;
+      const uint32_t cr = (lo & dk::ROT) ? C : 0u;
+      const uint32_t idc = (M + ((lo & dk::INC) ? 1u : 0u) + ((lo & dk::DEC) ? 0xFFu : 0u)) & 0xFFu;
+      const uint32_t r1 = (lo & dk::SHL) ? (((M << 1) | cr) & 0xFFu) : ((lo & dk::SHR) ? ((M >> 1) | (cr << 7)) : idc);
+      const uint32_t c1 = (lo & dk::SHL) ? (M >> 7) : ((lo & dk::SHR) ? (M & 1u) : C);
+      // unit2: logic / adder (ADC, SBC, CMP) / BIT
+      const uint32_t lhs = (hi & dk::CMP) ? R : A;
+      const uint32_t add = (hi & dk::INV) ? (r1 ^ 0xFFu) : r1;
+      const uint32_t sum = lhs + add + ((hi & dk::CMP) ? 1u : c1);
+      const uint32_t rlog = (hi & dk::OR) ? (A | r1) : ((hi & dk::AND) ? (A & r1) : (A ^ r1));
+      uint32_t r2 = (hi & dk::LOGIC) ? rlog : ((hi & dk::ARITH) ? (sum & 0xFFu) : r1);
+      uint32_t nC = (hi & dk::ARITH) ? (sum >> 8) : c1;
+      uint32_t nV = (hi & dk::ADDV) ? (((~(lhs ^ add) & (lhs ^ sum)) >> 7) & 1u)
+                                    : ((hi & dk::BIT) ? ((r1 >> 6) & 1u) : V);
+      uint32_t nn = (hi & dk::BIT) ? r1 : r2;
+      uint32_t nz_ = (hi & dk::BIT) ? (A & r1) : r2;
+      if (D && (hi & dk::ADDV)) decimal((hi & dk::INV) == 0, r1, c1, r2, nC, nV, nn, nz_);
+      if (lo & dk::WR) wr(c, ea, (lo & dk::WSEL) ? ((lo & dk::SAX) ? (A & X) : R) : r1);
+      A = (hi & dk::DA) ? r2 : A;
+      X = (hi & dk::DX) ? r2 : X;
+      Y = (hi & dk::DY) ? r2 : Y;
+      SP = (hi & dk::DS) ? r2 : SP;
+      nreg = (lo & dk::NZ) ? nn : nreg;
+      zreg = (lo & dk::NZ) ? (nz_ & 0xFFu) : zreg;
       C = nC;
       V = nV;
-      if ((lo32 >> dk::FOP) & 1u) {
-        const uint32_t fi = (lo32 >> dk::FIDX) & 3u, fv = (lo32 >> dk::FVAL) & 1u;
-        if (fi == 0) C = fv;
-        if (fi == 1) I = fv;
-        if (fi == 2) D = fv;
-        if (fi == 3) V = fv;
+      if (lo & dk::FOP) {
+        const uint32_t fi = (hi >> dk::FIDX) & 3u, fv = (hi & dk::FVAL) ? 1u : 0u;
+        C = fi == 0 ? fv : C;
+        I = fi == 1 ? fv : I;
+        D = fi == 2 ? fv : D;
+        V = fi == 3 ? fv : V;
       }
     }
 
-    // ---- end of instruction ----------------------------------------------------------------------
+    // ---- end of instruction ------------------------------------------------------------------------
     fc = now;
     t_phaseA = 3u * now;
     if (wsync_pending) fc = ((fc + 75u) / 76u) * 76u;  // stall to the next line start (R#5)
     if (fc >= c.cap_cycles) { fault = 2; return EV_FAULT; }  // fc / 76 >= line_cap
-    if (vsync_rose) return EV_FRAME;
-    return log_len > (uint32_t)(kLogCap - kLogMargin) ? EV_LOGFULL : EV_NONE;
+    return vsync_rose ? EV_FRAME : (log_len > (uint32_t)(kLogCap - kLogMargin) ? EV_LOGFULL : EV_NONE);
   }
 
   // NMOS decimal ADC / SBC (Bruce Clark's sequences, DESIGN.md §2 R#2)
-  __device__ __forceinline__ void decimal(uint32_t u2, uint32_t m, uint32_t cin, uint32_t& r2, uint32_t& nC,
+  __device__ __forceinline__ void decimal(bool is_adc, uint32_t m, uint32_t cin, uint32_t& r2, uint32_t& nC,
                                        uint32_t& nV, uint32_t& nn, uint32_t& nz_) const {
-    if (u2 == U2_ADC) {
+    if (is_adc) {
       uint32_t lo = (A & 0xFu) + (m & 0xFu) + cin;
       if (lo >= 0xAu) lo = ((lo + 6u) & 0xFu) + 0x10u;
       uint32_t s = (A & 0xF0u) + (m & 0xF0u) + lo;

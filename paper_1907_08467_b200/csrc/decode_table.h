@@ -4,11 +4,12 @@
 //
 // The kernel runs every ordinary instruction through ONE branch-free datapath:
 //   R  = register operand (A/X/Y/SP);  M = memory/immediate byte, or R for implied forms
-//   u1 = unit1(M): pass | ASL | LSR | ROL | ROR | INC | DEC   (carry c1)
-//   r2 = unit2(u1): pass | OR | AND | EOR | ADC | SBC | CMP(R) | BIT  (8-bit adder shared)
-//   then destination register, memory write value, N/Z/C/V updates — all selected by fields
-// so lanes executing different opcodes still share instructions.  Stack/control and the
-// rare undocumented immediates take a small "special" switch.
+//   r1 = unit1(M): pass | shift left | shift right (rotate: carry in) | +1 | -1   (carry c1)
+//   r2 = unit2(r1): pass | OR | AND | EOR | adder (ADC, SBC, CMP share it) | BIT
+//   then destination register(s), memory write value, N/Z/C/V updates.
+// Every control field is a one-hot flag bit, so each select compiles to a single predicate
+// test + SEL/LOP3 (multi-bit codes make the compiler emit compare-and-branch trees).
+// Stack/control and the rare undocumented immediates take a small "special" switch.
 //
 // Cycle counts derive from the addressing-mode x access-class rules of the NMOS 6502
 // (bottom table), not from a per-opcode list.
@@ -24,39 +25,61 @@ enum AddrMode : uint32_t {
   AM_IMP = 0, AM_ACC, AM_IMM, AM_ZP, AM_ZPX, AM_ZPY, AM_ABS, AM_ABSX, AM_ABSY, AM_IND,
   AM_INDX, AM_INDY, AM_REL
 };
-enum Unit1 : uint32_t { U1_PASS = 0, U1_ASL, U1_LSR, U1_ROL, U1_ROR, U1_INC, U1_DEC };
-enum Unit2 : uint32_t { U2_PASS = 0, U2_OR, U2_AND, U2_EOR, U2_ADC, U2_SBC, U2_CMP, U2_BIT };
-enum Reg : uint32_t { RG_A = 0, RG_X, RG_Y, RG_SP };
-enum Dst : uint32_t { DS_NONE = 0, DS_A, DS_X, DS_Y, DS_SP, DS_AX };
 enum Special : uint32_t {
   SP_NONE = 0, SP_PHA, SP_PHP, SP_PLA, SP_PLP, SP_JSR, SP_RTS, SP_RTI, SP_BRK, SP_ANC, SP_ALR,
   SP_ARR, SP_SBX, SP_JAM
 };
 
-// bit fields of an entry
+// ---- bit layout of an entry: low word (front end + unit1), high word (unit2 + write-back) ----
 namespace dk {
-constexpr int MODE = 0;     // 4 bits
-constexpr int LEN = 4;      // 2 bits: instruction length 1..3
-constexpr int CYC = 6;      // 4 bits: base cycles
-constexpr int PEN = 10;     // 1: +1 on page cross
-constexpr int RD = 11;      // 1: data read at EA
-constexpr int WR = 12;      // 1: data write at EA
-constexpr int RSRC = 13;    // 2: register operand R
-constexpr int OPR = 15;     // 1: M = R (implied/accumulator forms)
-constexpr int U1 = 16;      // 3
-constexpr int U2 = 19;      // 3
-constexpr int DST = 22;     // 3
-constexpr int WSEL = 25;    // 1: write value = store value (R, or A&X) instead of u1
-constexpr int SAX = 26;     // 1: store value A&X
-constexpr int NZ = 27;      // 1: update N/Z
-constexpr int FOP = 28;     // 1: flag set/clear op
-constexpr int FIDX = 29;    // 2: 0 C, 1 I, 2 D, 3 V
-constexpr int FVAL = 31;    // 1
-constexpr int SPC = 32;     // 4: special op
-constexpr int BR = 36;      // 1: conditional branch
-constexpr int BRF = 37;     // 2: branch flag 0 N 1 V 2 C 3 Z
-constexpr int BRT = 39;     // 1: taken when flag set
-constexpr int JMP = 40;     // 1: PC <- EA
+// low 32 bits
+constexpr uint32_t LEN = 0;      // 2 bits: instruction length 1..3
+constexpr uint32_t CYC = 2;      // 4 bits: base cycles
+constexpr uint32_t PEN = 1u << 6;   // +1 cycle on a page cross
+constexpr uint32_t RD = 1u << 7;    // data read at EA (phase C)
+constexpr uint32_t WR = 1u << 8;    // data write at EA (phase C)
+constexpr uint32_t ZP = 1u << 9;    // EA = zero-page address (zp, zp,X, zp,Y)
+constexpr uint32_t ZIX = 1u << 10;  // zero-page index X (zp,X and (zp,X))
+constexpr uint32_t ZIY = 1u << 11;  // zero-page index Y (zp,Y)
+constexpr uint32_t AIX = 1u << 12;  // 16-bit index X (abs,X)
+constexpr uint32_t AIY = 1u << 13;  // 16-bit index Y (abs,Y and (zp),Y)
+constexpr uint32_t PTRZ = 1u << 14; // pointer read from zero page ((zp,X), (zp),Y)
+constexpr uint32_t PTRA = 1u << 15; // pointer read with the page-wrap bug (JMP (abs))
+constexpr uint32_t BR = 1u << 16;   // conditional branch
+constexpr uint32_t JMP = 1u << 17;  // PC <- EA
+constexpr uint32_t RA = 1u << 18;   // register operand R = A
+constexpr uint32_t RX = 1u << 19;   // R = X
+constexpr uint32_t RY = 1u << 20;   // R = Y
+constexpr uint32_t RS = 1u << 21;   // R = SP
+constexpr uint32_t OPR = 1u << 22;  // M = R (implied / accumulator forms)
+constexpr uint32_t SHL = 1u << 23;  // unit1 shift left (ASL, ROL)
+constexpr uint32_t SHR = 1u << 24;  // unit1 shift right (LSR, ROR)
+constexpr uint32_t ROT = 1u << 25;  // carry into the vacated bit (ROL, ROR)
+constexpr uint32_t INC = 1u << 26;  // unit1 +1
+constexpr uint32_t DEC = 1u << 27;  // unit1 -1
+constexpr uint32_t NZ = 1u << 28;   // update N and Z
+constexpr uint32_t WSEL = 1u << 29; // write value = store value (R, or A&X) instead of r1
+constexpr uint32_t SAX = 1u << 30;  // store value A & X
+constexpr uint32_t FOP = 1u << 31;  // flag set/clear
+// high 32 bits
+constexpr uint32_t OR = 1u << 0;
+constexpr uint32_t AND = 1u << 1;
+constexpr uint32_t EOR = 1u << 2;
+constexpr uint32_t LOGIC = 1u << 3; // any of OR/AND/EOR
+constexpr uint32_t ADDV = 1u << 4;  // ADC or SBC: adder result to A, carry and overflow
+constexpr uint32_t INV = 1u << 5;   // adder operand inverted (SBC, CMP)
+constexpr uint32_t CMP = 1u << 6;   // adder: R - M with carry-in 1, result only to flags
+constexpr uint32_t BIT = 1u << 7;
+constexpr uint32_t ARITH = 1u << 8; // ADC, SBC or CMP
+constexpr uint32_t DA = 1u << 9;    // write r2 to A
+constexpr uint32_t DX = 1u << 10;
+constexpr uint32_t DY = 1u << 11;
+constexpr uint32_t DS = 1u << 12;
+constexpr uint32_t FIDX = 13;       // 2 bits: flag op target 0 C, 1 I, 2 D, 3 V
+constexpr uint32_t FVAL = 1u << 15;
+constexpr uint32_t SPC = 16;        // 4 bits: special op
+constexpr uint32_t BRF = 20;        // 2 bits: branch flag 0 N, 1 V, 2 C, 3 Z
+constexpr uint32_t BRT = 1u << 22;  // branch taken when the flag is set
 }  // namespace dk
 
 inline uint32_t mode_len(uint32_t mode) {
@@ -64,6 +87,20 @@ inline uint32_t mode_len(uint32_t mode) {
     case AM_IMP: case AM_ACC: return 1;
     case AM_ABS: case AM_ABSX: case AM_ABSY: case AM_IND: return 3;
     default: return 2;
+  }
+}
+
+inline uint32_t mode_bits(uint32_t mode) {
+  switch (mode) {
+    case AM_ZP: return dk::ZP;
+    case AM_ZPX: return dk::ZP | dk::ZIX;
+    case AM_ZPY: return dk::ZP | dk::ZIY;
+    case AM_ABSX: return dk::AIX;
+    case AM_ABSY: return dk::AIY;
+    case AM_IND: return dk::PTRA;
+    case AM_INDX: return dk::PTRZ | dk::ZIX;
+    case AM_INDY: return dk::PTRZ | dk::AIY;
+    default: return 0;
   }
 }
 
@@ -87,32 +124,24 @@ inline uint32_t mode_cycles(uint32_t mode, AccessClass cl, bool* pen) {
   }
 }
 
+// datapath fields of one operation (independent of the addressing mode)
 struct Micro {
-  uint32_t u1 = U1_PASS, u2 = U2_PASS, rsrc = RG_A, dst = DS_NONE;
-  bool opr = false, wsel = false, sax = false, nz = false;
+  uint32_t lo = 0;  // register operand / unit1 / NZ / write-value bits
+  uint32_t hi = 0;  // unit2 / destination bits
 };
 
 inline uint64_t entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr, const Micro& u) {
-  uint64_t e = 0;
-  e |= (uint64_t)mode << dk::MODE;
-  e |= (uint64_t)mode_len(mode) << dk::LEN;
-  e |= (uint64_t)cyc << dk::CYC;
-  e |= (uint64_t)(pen ? 1 : 0) << dk::PEN;
-  e |= (uint64_t)(rd ? 1 : 0) << dk::RD;
-  e |= (uint64_t)(wr ? 1 : 0) << dk::WR;
-  e |= (uint64_t)u.rsrc << dk::RSRC;
-  e |= (uint64_t)(u.opr ? 1 : 0) << dk::OPR;
-  e |= (uint64_t)u.u1 << dk::U1;
-  e |= (uint64_t)u.u2 << dk::U2;
-  e |= (uint64_t)u.dst << dk::DST;
-  e |= (uint64_t)(u.wsel ? 1 : 0) << dk::WSEL;
-  e |= (uint64_t)(u.sax ? 1 : 0) << dk::SAX;
-  e |= (uint64_t)(u.nz ? 1 : 0) << dk::NZ;
-  return e;
+  uint32_t lo = u.lo | mode_bits(mode) | (mode_len(mode) << dk::LEN) | (cyc << dk::CYC);
+  if (pen) lo |= dk::PEN;
+  if (rd) lo |= dk::RD;
+  if (wr) lo |= dk::WR;
+  return (uint64_t)lo | ((uint64_t)u.hi << 32);
 }
 
 inline void build_decode_table(uint64_t* table) {
-  for (int i = 0; i < 256; i++) table[i] = ((uint64_t)SP_JAM << dk::SPC) | (1ull << dk::LEN);
+  using namespace dk;
+  Micro nop;
+  for (int i = 0; i < 256; i++) table[i] = entry(AM_IMP, 2, false, false, false, nop) | ((uint64_t)SP_JAM << (32 + SPC));
   auto group = [&](const Micro& u, AccessClass cl, std::initializer_list<std::pair<uint32_t, uint32_t>> ms) {
     for (auto& p : ms) {
       bool pen;
@@ -122,66 +151,54 @@ inline void build_decode_table(uint64_t* table) {
       table[p.second] = entry(p.first, cyc, pen, rd, wr, u);
     }
   };
-  auto mk = [](uint32_t u1, uint32_t u2, uint32_t rsrc, uint32_t dst, bool nz) {
+  auto mk = [](uint32_t lo, uint32_t hi) {
     Micro m;
-    m.u1 = u1; m.u2 = u2; m.rsrc = rsrc; m.dst = dst; m.nz = nz;
+    m.lo = lo;
+    m.hi = hi;
     return m;
   };
-  // eight-mode ALU group aaa bbb 01
-  const uint32_t alu8[7][3] = {{U2_OR, 0x00, DS_A}, {U2_AND, 0x20, DS_A}, {U2_EOR, 0x40, DS_A},
-                               {U2_ADC, 0x60, DS_A}, {U2_PASS, 0xA0, DS_A}, {U2_CMP, 0xC0, DS_NONE},
-                               {U2_SBC, 0xE0, DS_A}};
+  const uint32_t adc = ADDV | ARITH, sbc = ADDV | INV | ARITH, cmp = CMP | INV | ARITH;
+  // eight-mode ALU group aaa bbb 01: ORA AND EOR ADC LDA CMP SBC
+  const uint32_t alu8[7][2] = {{OR | LOGIC | DA, 0x00}, {AND | LOGIC | DA, 0x20}, {EOR | LOGIC | DA, 0x40},
+                               {adc | DA, 0x60}, {DA, 0xA0}, {cmp, 0xC0}, {sbc | DA, 0xE0}};
   for (auto& g : alu8) {
     uint32_t b = g[1];
-    group(mk(U1_PASS, g[0], RG_A, g[2], true), CL_READ,
+    group(mk(RA | NZ, g[0]), CL_READ,
           {{AM_INDX, b + 0x01}, {AM_ZP, b + 0x05}, {AM_IMM, b + 0x09}, {AM_ABS, b + 0x0D},
            {AM_INDY, b + 0x11}, {AM_ZPX, b + 0x15}, {AM_ABSY, b + 0x19}, {AM_ABSX, b + 0x1D}});
   }
-  group(mk(U1_PASS, U2_SBC, RG_A, DS_A, true), CL_READ, {{AM_IMM, 0xEB}});
-  auto store = [&](uint32_t rsrc, bool sax) {
-    Micro m;
-    m.rsrc = rsrc; m.wsel = true; m.sax = sax;
-    return m;
-  };
-  group(store(RG_A, false), CL_WRITE, {{AM_INDX, 0x81}, {AM_ZP, 0x85}, {AM_ABS, 0x8D}, {AM_INDY, 0x91},
-                                       {AM_ZPX, 0x95}, {AM_ABSY, 0x99}, {AM_ABSX, 0x9D}});
-  group(store(RG_X, false), CL_WRITE, {{AM_ZP, 0x86}, {AM_ABS, 0x8E}, {AM_ZPY, 0x96}});
-  group(store(RG_Y, false), CL_WRITE, {{AM_ZP, 0x84}, {AM_ABS, 0x8C}, {AM_ZPX, 0x94}});
-  group(store(RG_A, true), CL_WRITE, {{AM_INDX, 0x83}, {AM_ZP, 0x87}, {AM_ABS, 0x8F}, {AM_ZPY, 0x97}});
-  group(mk(U1_PASS, U2_PASS, RG_A, DS_X, true), CL_READ,
-        {{AM_IMM, 0xA2}, {AM_ZP, 0xA6}, {AM_ABS, 0xAE}, {AM_ZPY, 0xB6}, {AM_ABSY, 0xBE}});
-  group(mk(U1_PASS, U2_PASS, RG_A, DS_Y, true), CL_READ,
-        {{AM_IMM, 0xA0}, {AM_ZP, 0xA4}, {AM_ABS, 0xAC}, {AM_ZPX, 0xB4}, {AM_ABSX, 0xBC}});
-  group(mk(U1_PASS, U2_PASS, RG_A, DS_AX, true), CL_READ,
+  group(mk(RA | NZ, sbc | DA), CL_READ, {{AM_IMM, 0xEB}});
+  group(mk(RA | WSEL, 0), CL_WRITE, {{AM_INDX, 0x81}, {AM_ZP, 0x85}, {AM_ABS, 0x8D}, {AM_INDY, 0x91},
+                                     {AM_ZPX, 0x95}, {AM_ABSY, 0x99}, {AM_ABSX, 0x9D}});
+  group(mk(RX | WSEL, 0), CL_WRITE, {{AM_ZP, 0x86}, {AM_ABS, 0x8E}, {AM_ZPY, 0x96}});
+  group(mk(RY | WSEL, 0), CL_WRITE, {{AM_ZP, 0x84}, {AM_ABS, 0x8C}, {AM_ZPX, 0x94}});
+  group(mk(RA | WSEL | SAX, 0), CL_WRITE, {{AM_INDX, 0x83}, {AM_ZP, 0x87}, {AM_ABS, 0x8F}, {AM_ZPY, 0x97}});
+  group(mk(NZ, DX), CL_READ, {{AM_IMM, 0xA2}, {AM_ZP, 0xA6}, {AM_ABS, 0xAE}, {AM_ZPY, 0xB6}, {AM_ABSY, 0xBE}});
+  group(mk(NZ, DY), CL_READ, {{AM_IMM, 0xA0}, {AM_ZP, 0xA4}, {AM_ABS, 0xAC}, {AM_ZPX, 0xB4}, {AM_ABSX, 0xBC}});
+  group(mk(NZ, DA | DX), CL_READ,
         {{AM_INDX, 0xA3}, {AM_ZP, 0xA7}, {AM_ABS, 0xAF}, {AM_INDY, 0xB3}, {AM_ZPY, 0xB7}, {AM_ABSY, 0xBF}});
-  group(mk(U1_PASS, U2_CMP, RG_X, DS_NONE, true), CL_READ, {{AM_IMM, 0xE0}, {AM_ZP, 0xE4}, {AM_ABS, 0xEC}});
-  group(mk(U1_PASS, U2_CMP, RG_Y, DS_NONE, true), CL_READ, {{AM_IMM, 0xC0}, {AM_ZP, 0xC4}, {AM_ABS, 0xCC}});
-  group(mk(U1_PASS, U2_BIT, RG_A, DS_NONE, true), CL_READ, {{AM_ZP, 0x24}, {AM_ABS, 0x2C}});
+  group(mk(RX | NZ, cmp), CL_READ, {{AM_IMM, 0xE0}, {AM_ZP, 0xE4}, {AM_ABS, 0xEC}});
+  group(mk(RY | NZ, cmp), CL_READ, {{AM_IMM, 0xC0}, {AM_ZP, 0xC4}, {AM_ABS, 0xCC}});
+  group(mk(RA | NZ, BIT), CL_READ, {{AM_ZP, 0x24}, {AM_ABS, 0x2C}});
   // shifts / rotates / inc / dec on memory, and the accumulator forms
-  const uint32_t rmw[6][2] = {{U1_ASL, 0x00}, {U1_ROL, 0x20}, {U1_LSR, 0x40}, {U1_ROR, 0x60},
-                              {U1_DEC, 0xC0}, {U1_INC, 0xE0}};
+  const uint32_t rmw[6][2] = {{SHL, 0x00}, {SHL | ROT, 0x20}, {SHR, 0x40}, {SHR | ROT, 0x60},
+                              {DEC, 0xC0}, {INC, 0xE0}};
   for (auto& g : rmw) {
     uint32_t b = g[1];
-    group(mk(g[0], U2_PASS, RG_A, DS_NONE, true), CL_RMW,
-          {{AM_ZP, b + 0x06}, {AM_ABS, b + 0x0E}, {AM_ZPX, b + 0x16}, {AM_ABSX, b + 0x1E}});
-    if (g[0] != U1_DEC && g[0] != U1_INC) {
-      Micro m = mk(g[0], U2_PASS, RG_A, DS_A, true);
-      m.opr = true;
-      table[b + 0x0A] = entry(AM_ACC, 2, false, false, false, m);
-    }
+    group(mk(g[0] | NZ, 0), CL_RMW, {{AM_ZP, b + 0x06}, {AM_ABS, b + 0x0E}, {AM_ZPX, b + 0x16}, {AM_ABSX, b + 0x1E}});
+    if (!(g[0] & (INC | DEC))) table[b + 0x0A] = entry(AM_ACC, 2, false, false, false, mk(g[0] | RA | OPR | NZ, DA));
   }
-  // undocumented RMW combinations (unit1 on memory, unit2 into A)
-  const uint32_t urmw[6][4] = {{U1_ASL, U2_OR, 0x00, DS_A}, {U1_ROL, U2_AND, 0x20, DS_A},
-                               {U1_LSR, U2_EOR, 0x40, DS_A}, {U1_ROR, U2_ADC, 0x60, DS_A},
-                               {U1_DEC, U2_CMP, 0xC0, DS_NONE}, {U1_INC, U2_SBC, 0xE0, DS_A}};
+  // undocumented RMW combinations: unit1 on memory, unit2 into A (DCP compares)
+  const uint32_t urmw[6][3] = {{SHL, OR | LOGIC | DA, 0x00}, {SHL | ROT, AND | LOGIC | DA, 0x20},
+                               {SHR, EOR | LOGIC | DA, 0x40}, {SHR | ROT, adc | DA, 0x60},
+                               {DEC, cmp, 0xC0}, {INC, sbc | DA, 0xE0}};
   for (auto& g : urmw) {
     uint32_t b = g[2];
-    group(mk(g[0], g[1], RG_A, g[3], true), CL_RMW,
+    group(mk(g[0] | RA | NZ, g[1]), CL_RMW,
           {{AM_INDX, b + 0x03}, {AM_ZP, b + 0x07}, {AM_ABS, b + 0x0F}, {AM_INDY, b + 0x13},
            {AM_ZPX, b + 0x17}, {AM_ABSY, b + 0x1B}, {AM_ABSX, b + 0x1F}});
   }
   // NOPs (the reading forms perform their data read)
-  Micro nop;
   for (uint32_t o : {0xEAu, 0x1Au, 0x3Au, 0x5Au, 0x7Au, 0xDAu, 0xFAu}) table[o] = entry(AM_IMP, 2, false, false, false, nop);
   group(nop, CL_READ, {{AM_IMM, 0x80}, {AM_IMM, 0x82}, {AM_IMM, 0x89}, {AM_IMM, 0xC2}, {AM_IMM, 0xE2},
                        {AM_ZP, 0x04}, {AM_ZP, 0x44}, {AM_ZP, 0x64}, {AM_ABS, 0x0C},
@@ -189,38 +206,34 @@ inline void build_decode_table(uint64_t* table) {
                        {AM_ZPX, 0xF4}, {AM_ABSX, 0x1C}, {AM_ABSX, 0x3C}, {AM_ABSX, 0x5C},
                        {AM_ABSX, 0x7C}, {AM_ABSX, 0xDC}, {AM_ABSX, 0xFC}});
   // register increments / transfers: M = R
-  auto reg = [&](uint32_t opc, uint32_t u1, uint32_t rsrc, uint32_t dst, bool nz) {
-    Micro m = mk(u1, U2_PASS, rsrc, dst, nz);
-    m.opr = true;
-    table[opc] = entry(AM_IMP, 2, false, false, false, m);
+  auto reg = [&](uint32_t opc, uint32_t lo, uint32_t hi) {
+    table[opc] = entry(AM_IMP, 2, false, false, false, mk(lo | OPR, hi));
   };
-  reg(0xE8, U1_INC, RG_X, DS_X, true);   // INX
-  reg(0xC8, U1_INC, RG_Y, DS_Y, true);   // INY
-  reg(0xCA, U1_DEC, RG_X, DS_X, true);   // DEX
-  reg(0x88, U1_DEC, RG_Y, DS_Y, true);   // DEY
-  reg(0xAA, U1_PASS, RG_A, DS_X, true);  // TAX
-  reg(0xA8, U1_PASS, RG_A, DS_Y, true);  // TAY
-  reg(0x8A, U1_PASS, RG_X, DS_A, true);  // TXA
-  reg(0x98, U1_PASS, RG_Y, DS_A, true);  // TYA
-  reg(0xBA, U1_PASS, RG_SP, DS_X, true); // TSX
-  reg(0x9A, U1_PASS, RG_X, DS_SP, false);// TXS
+  reg(0xE8, RX | INC | NZ, DX);  // INX
+  reg(0xC8, RY | INC | NZ, DY);  // INY
+  reg(0xCA, RX | DEC | NZ, DX);  // DEX
+  reg(0x88, RY | DEC | NZ, DY);  // DEY
+  reg(0xAA, RA | NZ, DX);        // TAX
+  reg(0xA8, RA | NZ, DY);        // TAY
+  reg(0x8A, RX | NZ, DA);        // TXA
+  reg(0x98, RY | NZ, DA);        // TYA
+  reg(0xBA, RS | NZ, DX);        // TSX
+  reg(0x9A, RX, DS);             // TXS
   // flag set/clear: (opcode, flag index C=0 I=1 D=2 V=3, value)
   const uint32_t fl[7][3] = {{0x18, 0, 0}, {0x38, 0, 1}, {0x58, 1, 0}, {0x78, 1, 1},
                              {0xB8, 3, 0}, {0xD8, 2, 0}, {0xF8, 2, 1}};
   for (auto& f : fl)
-    table[f[0]] = entry(AM_IMP, 2, false, false, false, nop) | (1ull << dk::FOP) |
-                  ((uint64_t)f[1] << dk::FIDX) | ((uint64_t)f[2] << dk::FVAL);
+    table[f[0]] = entry(AM_IMP, 2, false, false, false, mk(FOP, (f[1] << FIDX) | (f[2] ? FVAL : 0u)));
   // control flow
-  table[0x4C] = entry(AM_ABS, 3, false, false, false, nop) | (1ull << dk::JMP);
-  table[0x6C] = entry(AM_IND, 5, false, false, false, nop) | (1ull << dk::JMP);
+  table[0x4C] = entry(AM_ABS, 3, false, false, false, mk(JMP, 0));
+  table[0x6C] = entry(AM_IND, 5, false, false, false, mk(JMP, 0));
   const uint32_t br[8][3] = {{0x10, 0, 0}, {0x30, 0, 1}, {0x50, 1, 0}, {0x70, 1, 1},
                              {0x90, 2, 0}, {0xB0, 2, 1}, {0xD0, 3, 0}, {0xF0, 3, 1}};
   for (auto& b : br)
-    table[b[0]] = entry(AM_REL, 2, false, false, false, nop) | (1ull << dk::BR) |
-                  ((uint64_t)b[1] << dk::BRF) | ((uint64_t)b[2] << dk::BRT);
+    table[b[0]] = entry(AM_REL, 2, false, false, false, mk(BR, (b[1] << BRF) | (b[2] ? BRT : 0u)));
   // specials: stack/control and the immediate-only undocumented ops
   auto spc = [&](uint32_t opc, uint32_t mode, uint32_t cyc, uint32_t s) {
-    table[opc] = entry(mode, cyc, false, false, false, nop) | ((uint64_t)s << dk::SPC);
+    table[opc] = entry(mode, cyc, false, false, false, nop) | ((uint64_t)s << (32 + SPC));
   };
   spc(0x48, AM_IMP, 3, SP_PHA);
   spc(0x08, AM_IMP, 3, SP_PHP);

@@ -17,6 +17,11 @@
 
 namespace cule {
 
+// min resident blocks of 128 threads per SM for the step/debug kernels (register budget)
+#ifndef CULE_MINB
+#define CULE_MINB 1
+#endif
+
 enum RunStatus : int32_t { RUN_BUDGET = 0, RUN_JAM = 1, RUN_RUNAWAY = 2, RUN_FRAME = 3 };
 constexpr uint32_t EV_BUDGET = 4;
 constexpr uint32_t kFull = 0xFFFFFFFFu;
@@ -350,7 +355,7 @@ __device__ __forceinline__ void warp_zero(uint8_t* p, uint32_t bytes, uint32_t l
 }
 
 template <bool kGray>
-__global__ void __launch_bounds__(128) step_kernel(Params p) {
+__global__ void __launch_bounds__(128, CULE_MINB) step_kernel(Params p) {
   extern __shared__ __align__(16) uint8_t smem[];
   const Ctx c = stage_block(p, smem, kGray);
   uint32_t i = 0;
