@@ -156,8 +156,7 @@ struct Cpu {
     }
     const uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
     const uint32_t spc = (hi >> dk::SPC) & 0xFu;
-    if (spc == SP_JAM) { PC = (pc + 1) & 0xFFFFu; fault = 1; return EV_FAULT; }
-    uint32_t n = (lo >> dk::CYC) & 0xFu;
+    uint32_t n = (lo >> dk::CYC) & 0xFu;  // JAM entries: 1 byte, 0 cycles, no effects (R#1)
     PC = (pc + (lo & 3u)) & 0xFFFFu;
 
     // ---- phase A: effective address --------------------------------------------------------------
@@ -188,10 +187,9 @@ struct Cpu {
     uint32_t v = b1;  // immediate operand
     if (lo & dk::RD) v = rd<false>(c, ea);
 
-    if (spc) {
-      special(c, spc, v, ea);
-    } else {
-      // register operand and unit1 (shift / rotate / increment)
+    {
+      // register operand and unit1 (shift / rotate / increment); special ops have no unit bits,
+      // so this datapath leaves their state unchanged and the special switch runs after it
       const uint32_t R = ((lo & dk::RA) ? A : 0u) | ((lo & dk::RX) ? X : 0u) | ((lo & dk::RY) ? Y : 0u) |
                          ((lo & dk::RS) ? SP : 0u);
       const uint32_t M = (lo & dk::OPR) ? R : v;
@@ -228,13 +226,15 @@ struct Cpu {
         V = fi == 3 ? fv : V;
       }
     }
+    if (spc) special(c, spc, v, ea);
 
     // ---- end of instruction ------------------------------------------------------------------------
     fc = now;
     t_phaseA = 3u * now;
     if (wsync_pending) fc = ((fc + 75u) / 76u) * 76u;  // stall to the next line start (R#5)
-    if (fc >= c.cap_cycles) { fault = 2; return EV_FAULT; }  // fc / 76 >= line_cap
-    return vsync_rose ? EV_FRAME : (log_len > (uint32_t)(kLogCap - kLogMargin) ? EV_LOGFULL : EV_NONE);
+    fault = (fc >= c.cap_cycles && !fault) ? 2u : fault;  // runaway: fc / 76 >= line_cap
+    return fault ? EV_FAULT
+                 : (vsync_rose ? EV_FRAME : (log_len > (uint32_t)(kLogCap - kLogMargin) ? EV_LOGFULL : EV_NONE));
   }
 
   // NMOS decimal ADC / SBC (Bruce Clark's sequences, DESIGN.md §2 R#2)
@@ -304,6 +304,7 @@ struct Cpu {
         V = ((A >> 6) ^ (A >> 5)) & 1u;
       } break;
       case SP_SBX: { uint32_t t = A & X; C = t >= v ? 1u : 0u; X = (t - v) & 0xFFu; nreg = X; zreg = X; } break;
+      case SP_JAM: fault = 1; break;
       default: break;
     }
   }

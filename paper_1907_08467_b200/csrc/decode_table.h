@@ -141,7 +141,8 @@ inline uint64_t entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr, c
 inline void build_decode_table(uint64_t* table) {
   using namespace dk;
   Micro nop;
-  for (int i = 0; i < 256; i++) table[i] = entry(AM_IMP, 2, false, false, false, nop) | ((uint64_t)SP_JAM << (32 + SPC));
+  // JAM / unstable: the opcode fetch happens (1 byte), then the env faults with fc unchanged
+  for (int i = 0; i < 256; i++) table[i] = entry(AM_IMP, 0, false, false, false, nop) | ((uint64_t)SP_JAM << (32 + SPC));
   auto group = [&](const Micro& u, AccessClass cl, std::initializer_list<std::pair<uint32_t, uint32_t>> ms) {
     for (auto& p : ms) {
       bool pen;
