@@ -262,6 +262,33 @@ def test_num_envs_and_step_host_equivalence():
     assert (big.get_state()[:20] == small.get_state()).all()
 
 
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4"])
+def test_sampled_parity_at_full_size(cfg):
+    """cfg3 (16384 envs, F8 ROM R2) and cfg4 (32768 envs, R1-R4 interleaved) at full size in the
+    bench's launch configuration (default envs-per-warp heuristic, ROM-grouped lanes); sampled
+    envs replayed in the oracle with their global ids, including the last env (ragged tail)."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    names, N = (["R2"], 16384) if cfg == "cfg3" else (["R1", "R2", "R3", "R4"], 32768)
+    roms = [games.build_rom(n) for n in names]
+    steps = 8
+    gpu = Env(roms, N, 4)
+    gpu.reset(0)
+    acts = H.random_actions(N, steps, 99)
+    rng = np.random.default_rng(1)
+    sample = np.unique(np.concatenate([np.arange(0, 9), [N // 2 - 1, N // 2, N - 2, N - 1],
+                                       rng.integers(0, N, 19)]))
+    ref = oracle.OracleEnv(roms, len(sample), 4, H.palette_rgb())
+    ref.set_env_ids(sample)
+    ref.reset(0)
+    for t in range(steps):
+        o, r, d = gpu.step(torch.from_numpy(acts[t]).cuda())
+        o2, r2, d2 = ref.step(acts[t][sample])
+        assert (o.cpu().numpy()[sample] == o2).all(), t
+        assert (r.cpu().numpy()[sample] == r2).all() and (d.cpu().numpy()[sample] == d2).all()
+    assert_same_state(gpu.get_state()[sample], ref.get_state(), f"{cfg} sample")
+
+
 def test_sampled_parity_at_cfg2_size():
     """cfg2 at full size (4096 envs, R1, fs=4, GRAY84, default K=30) in the bench's launch
     configuration; 48 sampled envs replayed one by one in the oracle."""
