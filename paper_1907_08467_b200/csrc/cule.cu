@@ -14,6 +14,8 @@
 #include "../../include/cule.h"
 #include "decode_table.h"
 #include "kernels.cuh"
+#include "scalar_decode.h"
+#include "scalar_kernels.cuh"
 
 namespace {
 
@@ -29,7 +31,7 @@ int fail(int code, const std::string& msg) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t state, pack, staging, cstate, cobs, cscore, cstage, roms, decode, gray, counters, err,
+  size_t state, pack, staging, cstate, cobs, cscore, cstage, roms, decode, sdecode, gray, counters, err,
       io_act, io_obs, io_rew, io_done, total;
 };
 
@@ -52,6 +54,7 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   L->cstage = take(gray ? 2 * nk * cule::kFrameBytes : 0);
   L->roms = take(4 * 8192);
   L->decode = take(2048);
+  L->sdecode = take(1024);
   L->gray = take(128);
   L->counters = take(32);
   L->err = take(16);
@@ -77,6 +80,8 @@ struct cule_env {
   size_t smem;
   uint32_t block;
   uint32_t epw;            // envs per warp
+  int engine;              // 0 batched (SIMT datapath, epw envs per warp), 1 scalar (one env per warp)
+  size_t ssmem;            // dynamic shared memory of the scalar kernels
   uint32_t slot_start[4], first_env[4];
   uint32_t grid;           // blocks of the step / debug kernels
 };
@@ -93,6 +98,7 @@ static cule::Params base_params(const cule_env* e) {
   p.f8_mask = e->f8_mask;
   p.n_roms = (uint32_t)e->n_roms;
   p.decode = reinterpret_cast<const uint64_t*>(e->ws + e->L.decode);
+  p.sdecode = reinterpret_cast<const uint32_t*>(e->ws + e->L.sdecode);
   p.gray = e->ws + e->L.gray;
   p.cache_state = e->ws + e->L.cstate;
   p.cache_score = reinterpret_cast<const uint16_t*>(e->ws + e->L.cscore);
@@ -141,6 +147,17 @@ static int sm_count() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return sms;
+}
+
+// Engine: the scalar engine (one env per warp, compact interpreter, warp-cooperative TIA)
+// wins at low env counts, the batched engine (SIMT datapath) at high ones.  CULE_ENGINE
+// overrides (simt | scalar).
+static int choose_engine(int N) {
+  if (const char* v = getenv("CULE_ENGINE")) {
+    if (!strcmp(v, "simt")) return 0;
+    if (!strcmp(v, "scalar")) return 1;
+  }
+  return 0;  // default engine until the scalar engine is validated on the GPU
 }
 
 // Envs per warp: the per-env 6502 chain is latency-bound, so at low env counts the kernel
@@ -246,6 +263,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   }
   e->rom_bytes = off;
   e->epw = choose_epw(num_envs);
+  e->engine = choose_engine(num_envs);
+  e->ssmem = cule::scalar_smem_bytes(e->rom_bytes);
   {
     const uint32_t warps = ((uint32_t)num_envs + e->epw - 1) / e->epw;
     e->block = choose_block(warps);
@@ -269,6 +288,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   for (int r = 0; r < n_roms; ++r) std::memcpy(romimg + e->rom_off[r], roms[r], rom_lens[r]);
   uint64_t table[256];
   cule::build_decode_table(table);
+  uint32_t stable[256];
+  cule::build_scalar_table(stable);
   uint8_t gray[128] = {0};
   if (cfg->palette_rgb) {
     for (int i = 0; i < 128; ++i) {
@@ -278,6 +299,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   }
   cudaMemcpy(e->ws + L.roms, romimg, e->rom_bytes, cudaMemcpyHostToDevice);
   cudaMemcpy(e->ws + L.decode, table, sizeof table, cudaMemcpyHostToDevice);
+  cudaMemcpy(e->ws + L.sdecode, stable, sizeof stable, cudaMemcpyHostToDevice);
   cudaMemcpy(e->ws + L.gray, gray, sizeof gray, cudaMemcpyHostToDevice);
   cudaMemset(e->ws + L.state, 0, 256 * (size_t)num_envs);
   cudaMemset(e->ws + L.counters, 0, 32);
@@ -291,6 +313,9 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   cudaFuncSetAttribute(cule::cache_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
   cudaFuncSetAttribute(cule::cache_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
   cudaFuncSetAttribute(cule::debug_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+  cudaFuncSetAttribute(cule::scalar_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->ssmem);
+  cudaFuncSetAttribute(cule::scalar_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->ssmem);
+  cudaFuncSetAttribute(cule::scalar_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->ssmem);
 
   // reset cache build: one thread per (rom, entry)
   cule::Params p = base_params(e);
@@ -339,8 +364,15 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
   p.obs = static_cast<uint8_t*>(d_obs);
   p.rewards = d_rewards;
   p.dones = d_dones;
-  if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::step_kernel<true><<<e->grid, e->block, e->smem, s>>>(p);
-  else cule::step_kernel<false><<<e->grid, e->block, e->smem, s>>>(p);
+  if (e->engine == 1) {
+    const uint32_t sg = ((uint32_t)e->N + cule::kSWarps - 1) / cule::kSWarps;
+    if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::scalar_kernel<true, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
+    else cule::scalar_kernel<false, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
+  } else if (e->cfg.obs_mode == CULE_OBS_GRAY84) {
+    cule::step_kernel<true><<<e->grid, e->block, e->smem, s>>>(p);
+  } else {
+    cule::step_kernel<false><<<e->grid, e->block, e->smem, s>>>(p);
+  }
   return cuda_check("step_kernel");
 }
 
@@ -407,7 +439,12 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
   cule::Params p = base_params(e);
   p.debug_instr = n_instr;
   p.debug_status = d_status;
-  cule::debug_kernel<<<e->grid, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
+  if (e->engine == 1) {
+    const uint32_t sg = ((uint32_t)e->N + cule::kSWarps - 1) / cule::kSWarps;
+    cule::scalar_kernel<false, true><<<sg, 32 * cule::kSWarps, e->ssmem, static_cast<cudaStream_t>(stream)>>>(p);
+  } else {
+    cule::debug_kernel<<<e->grid, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
+  }
   return cuda_check("debug_kernel");
 }
 

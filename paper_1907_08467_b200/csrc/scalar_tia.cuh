@@ -1,0 +1,311 @@
+// scalar_tia.cuh — warp-cooperative TIA replay for the scalar engine (one env per warp).
+//
+// The replay of one env's write log is sequential in time, but within a span of colour clocks
+// with constant registers the work is parallel in x ("the TIA kernel may be
+// scheduled ... with more than one thread per game, as rendering of diverse rows on the screen
+// is indeed a parallel operation").  All 32 lanes of the env's warp replay the log together:
+// the TIA registers are warp-uniform and kept PACKED in the nine words of the shared-memory
+// layout (tia.cuh Tia::load/store), fields extracted on use, so the replay stays within the
+// scalar engine's register budget; lane j < 10 owns 16-pixel chunk j of the row being
+// assembled and computes its pixels once per span; even lanes 0..8 own 32-pixel coverage word
+// j/2 for collisions, OR-reduced across the warp; a completed row leaves as ten coalesced
+// 16-byte stores.  Same written model as tia.cuh (DESIGN.md §2 R#7-R#14), independent code.
+#pragma once
+#include "tia.cuh"
+
+namespace cule {
+
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return (w >> (8 * i)) & 0xFFu; }
+__device__ __forceinline__ uint32_t with_byte(uint32_t w, int i, uint32_t v) {
+  return (w & ~(0xFFu << (8 * i))) | ((v & 0xFFu) << (8 * i));
+}
+
+// TIA registers, packed: the nine shared-memory words
+//   w0 COLUP0 COLUP1 COLUPF COLUBK | w1 PF0 PF1 PF2 CTRLPF | w2 NUSIZ0 NUSIZ1 GRP0new GRP0old
+//   w3 GRP1new GRP1old HMP0 HMP1   | w4 HMM0 HMM1 HMBL     | w5 flags(16) comb_line(16)
+//   w6 posP0 posP1 posM0 posM1     | w7 posBL, collisions(16) << 16 | t = colour clock
+struct TiaP {
+  uint32_t w0, w1, w2, w3, w4, w5, w6, w7, t;
+
+  __device__ __forceinline__ uint32_t f(int b) const { return (w5 >> b) & 1u; }
+  __device__ __forceinline__ void setf(int b, uint32_t v) { w5 = (w5 & ~(1u << b)) | ((v & 1u) << b); }
+  __device__ __forceinline__ uint32_t coll() const { return w7 >> 16; }
+  __device__ __forceinline__ int32_t comb_line() const { return (int32_t)(int16_t)(w5 >> 16); }
+  __device__ __forceinline__ void load(const uint32_t* tw) {
+    w0 = tw[0]; w1 = tw[1]; w2 = tw[2]; w3 = tw[3]; w4 = tw[4]; w5 = tw[5]; w6 = tw[6]; w7 = tw[7]; t = tw[8];
+  }
+  __device__ __forceinline__ void store(uint32_t* tw) const {
+    tw[0] = w0; tw[1] = w1; tw[2] = w2; tw[3] = w3; tw[4] = w4; tw[5] = w5; tw[6] = w6; tw[7] = w7; tw[8] = t;
+  }
+  __device__ __forceinline__ uint32_t grp0() const { return byte_of(w2, f(7) ? 3 : 2); }
+  __device__ __forceinline__ uint32_t grp1() const { return byte_of(w3, f(8) ? 1 : 0); }
+  __device__ __forceinline__ uint32_t ball_on() const { return f(9) ? f(6) : f(5); }
+
+  // collision latches the objects present now could still set (an absent object cannot collide)
+  __device__ __forceinline__ uint32_t open_pairs() const {
+    const uint32_t p0 = grp0() != 0u, p1 = grp1() != 0u;
+    const uint32_t m0 = f(3) & (f(10) ^ 1u), m1 = f(4) & (f(11) ^ 1u);
+    const uint32_t bl = ball_on();
+    const uint32_t pf = (w1 & 0x00FFFFF0u) != 0u;  // PF0 D4-D7, PF1, PF2
+    const uint32_t possible = (m0 & p1) | ((m0 & p0) << 1) | ((m1 & p0) << 2) | ((m1 & p1) << 3) |
+                              ((p0 & pf) << 4) | ((p0 & bl) << 5) | ((p1 & pf) << 6) | ((p1 & bl) << 7) |
+                              ((m0 & pf) << 8) | ((m0 & bl) << 9) | ((m1 & pf) << 10) | ((m1 & bl) << 11) |
+                              ((bl & pf) << 12) | ((p0 & p1) << 14) | ((m0 & m1) << 15);
+    return possible & ~coll();
+  }
+
+  // apply a logged write at colour clock T (DESIGN.md §2 R#7-R#12)
+  __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T) {
+    const uint32_t line = T / 228u, h = T - line * 228u;
+    const int32_t hp = (int32_t)h - 68;
+    switch (r) {
+      case 0x01: setf(0, v >> 1); break;
+      case 0x04: w2 = with_byte(w2, 0, v); break;
+      case 0x05: w2 = with_byte(w2, 1, v); break;
+      case 0x06: case 0x07: case 0x08: case 0x09: w0 = with_byte(w0, (int)(r - 6u), v); break;
+      case 0x0A: w1 = with_byte(w1, 3, v); break;
+      case 0x0B: setf(1, v >> 3); break;
+      case 0x0C: setf(2, v >> 3); break;
+      case 0x0D: case 0x0E: case 0x0F: w1 = with_byte(w1, (int)(r - 0x0Du), v); break;
+      case 0x10: case 0x11: case 0x12: case 0x13: case 0x14: {  // RESP0/1, RESM0/1, RESBL
+        const uint32_t base = r <= 0x11u ? 5u : 4u;
+        const uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
+        if (r == 0x14u) w7 = with_byte(w7, 0, p);
+        else w6 = with_byte(w6, (int)(r - 0x10u), p);
+      } break;
+      case 0x1B: w2 = with_byte(w2, 2, v); w3 = with_byte(w3, 1, byte_of(w3, 0)); break;  // GRP0; GRP1 old <- new
+      case 0x1C:  // GRP1; GRP0 old <- new; ENABL old <- new
+        w3 = with_byte(w3, 0, v);
+        w2 = with_byte(w2, 3, byte_of(w2, 2));
+        setf(6, f(5));
+        break;
+      case 0x1D: setf(3, v >> 1); break;
+      case 0x1E: setf(4, v >> 1); break;
+      case 0x1F: setf(5, v >> 1); break;
+      case 0x20: w3 = with_byte(w3, 2, v >> 4); break;
+      case 0x21: w3 = with_byte(w3, 3, v >> 4); break;
+      case 0x22: case 0x23: case 0x24: w4 = with_byte(w4, (int)(r - 0x22u), v >> 4); break;
+      case 0x25: setf(7, v); break;
+      case 0x26: setf(8, v); break;
+      case 0x27: setf(9, v); break;
+      case 0x28: case 0x29: {  // RESMP: the missile locks to its player's centre on release
+        const int b = r == 0x28u ? 10 : 11;
+        const uint32_t nv = (v >> 1) & 1u;
+        if (f(b) && !nv) {
+          const uint32_t md = byte_of(w2, r == 0x28u ? 0 : 1) & 7u;
+          const uint32_t c = md == 5u ? 6u : (md == 7u ? 10u : 3u);
+          const uint32_t pp = byte_of(w6, r == 0x28u ? 0 : 1);
+          w6 = with_byte(w6, r == 0x28u ? 2 : 3, (pp + c) % 160u);
+        }
+        setf(b, nv);
+      } break;
+      case 0x2A: {  // HMOVE
+        auto mv = [](uint32_t p, uint32_t hm) -> uint32_t {
+          const int32_t q = (int32_t)p - ((int32_t)(hm ^ 8u) - 8);
+          return (uint32_t)(q < 0 ? q + 160 : (q >= 160 ? q - 160 : q));
+        };
+        const uint32_t p0 = mv(byte_of(w6, 0), byte_of(w3, 2)), p1 = mv(byte_of(w6, 1), byte_of(w3, 3));
+        const uint32_t m0 = mv(byte_of(w6, 2), byte_of(w4, 0)), m1 = mv(byte_of(w6, 3), byte_of(w4, 1));
+        w6 = p0 | (p1 << 8) | (m0 << 16) | (m1 << 24);
+        w7 = with_byte(w7, 0, mv(byte_of(w7, 0), byte_of(w4, 2)));
+        if (h < 68u) w5 = (w5 & 0xFFFFu) | ((line & 0xFFFFu) << 16);
+      } break;
+      case 0x2B: w3 &= 0x0000FFFFu; w4 = 0u; break;  // HMCLR
+      case 0x2C: w7 &= 0xFFFFu; break;               // CXCLR
+      default: break;
+    }
+  }
+};
+
+// word k (pixels 32k..32k+31) of a <=32-bit pattern placed at pos + copy offsets (circular 160)
+__device__ __forceinline__ uint32_t obj_word(uint32_t k, uint32_t pat, uint32_t pos, uint32_t cps) {
+  uint32_t w = 0u;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (!((cps >> c) & 1u)) continue;
+    uint32_t p = pos + (c == 0 ? 0u : (8u << c));
+    if (p >= 160u) p -= 160u;
+    int32_t d = (int32_t)p - (int32_t)(32u * k);
+    if (d < 0) d += 160;
+    if (d < 32) w |= pat << d;
+    if (d > 128) w |= pat >> (160 - d);
+  }
+  return w;
+}
+
+// coverage of the six objects in word k
+struct Words { uint32_t p0, p1, m0, m1, bl, pf; };
+
+__device__ __forceinline__ uint32_t player_word(uint32_t k, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl) {
+  if (g == 0u) return 0u;
+  const uint32_t mode = nusiz & 7u;
+  uint32_t pat = refl ? g : rev8(g);  // pixel d shows graphic bit 7-d (bit d when reflected)
+  if (mode == 5u) pat = spread2(pat);
+  else if (mode == 7u) pat = spread4(pat);
+  return obj_word(k, pat, pos, Tia::copies(mode));
+}
+__device__ __forceinline__ uint32_t missile_word(uint32_t k, uint32_t pos, uint32_t nusiz, bool en) {
+  if (!en) return 0u;
+  const uint32_t mode = nusiz & 7u;
+  const uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3u))) - 1u;
+  return obj_word(k, pat, pos, (mode == 5u || mode == 7u) ? 1u : Tia::copies(mode));
+}
+
+__device__ __forceinline__ Words object_words(const TiaP& t, uint32_t k) {
+  Words w;
+  w.p0 = player_word(k, byte_of(t.w6, 0), byte_of(t.w2, 0), t.grp0(), t.f(1));
+  w.p1 = player_word(k, byte_of(t.w6, 1), byte_of(t.w2, 1), t.grp1(), t.f(2));
+  w.m0 = missile_word(k, byte_of(t.w6, 2), byte_of(t.w2, 0), t.f(3) && !t.f(10));
+  w.m1 = missile_word(k, byte_of(t.w6, 3), byte_of(t.w2, 1), t.f(4) && !t.f(11));
+  w.bl = t.ball_on() ? obj_word(k, (1u << (1u << ((byte_of(t.w1, 3) >> 4) & 3u))) - 1u, byte_of(t.w7, 0), 1u) : 0u;
+  // playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), each 4 pixels wide
+  const uint32_t left = ((byte_of(t.w1, 0) >> 4) & 0xFu) | (rev8(byte_of(t.w1, 1)) << 4) | (byte_of(t.w1, 2) << 12);
+  const uint32_t right = (t.w1 & 0x01000000u) ? (__brev(left) >> 12) : left;
+  const uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
+  w.pf = spread4((uint32_t)(cells >> (8u * k)));
+  return w;
+}
+
+// the row being assembled: lane j < 10 holds chunk j (pixels 16j..16j+15)
+struct RowBuf {
+  uint32_t r0, r1, r2, r3;
+  uint32_t row;       // warp-uniform: window row held (rows before it are stored)
+  uint32_t fill;      // black, replicated (palette 0 or gray[0])
+  uint8_t* frame;     // 33,600-byte frame of this env
+  bool render;
+};
+
+// collision bits of visible pixels [xa, xb) reduced over the warp (even lanes 0..8 hold word lane/2)
+__device__ __forceinline__ uint32_t collide_coop(const Words& w, uint32_t lane, uint32_t xa, uint32_t xb) {
+  uint32_t bits = 0u;
+  if (lane < 10u && !(lane & 1u)) {
+    const uint32_t lo = 16u * lane;
+    const uint32_t s = xa > lo ? min(xa - lo, 32u) : 0u, e = xb > lo ? min(xb - lo, 32u) : 0u;
+    const uint32_t r = e > s ? ((e - s == 32u ? 0xFFFFFFFFu : ((1u << (e - s)) - 1u)) << s) : 0u;
+    const uint32_t p0 = w.p0 & r, p1 = w.p1 & r, m0 = w.m0 & r, m1 = w.m1 & r, bl = w.bl & r, pf = w.pf & r;
+    bits = ((m0 & p1) ? 1u : 0u) | ((m0 & p0) ? 2u : 0u) | ((m1 & p0) ? 4u : 0u) | ((m1 & p1) ? 8u : 0u) |
+           ((p0 & pf) ? 0x10u : 0u) | ((p0 & bl) ? 0x20u : 0u) | ((p1 & pf) ? 0x40u : 0u) |
+           ((p1 & bl) ? 0x80u : 0u) | ((m0 & pf) ? 0x100u : 0u) | ((m0 & bl) ? 0x200u : 0u) |
+           ((m1 & pf) ? 0x400u : 0u) | ((m1 & bl) ? 0x800u : 0u) | ((bl & pf) ? 0x1000u : 0u) |
+           ((p0 & p1) ? 0x4000u : 0u) | ((m0 & m1) ? 0x8000u : 0u);
+  }
+  return __reduce_or_sync(0xFFFFFFFFu, bits);
+}
+
+// the 16 pixels of the lane's chunk (4 words of 4 bytes) with the registers of the current span
+__device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t lane, const uint8_t* gray,
+                                         uint32_t& x0w, uint32_t& x1w, uint32_t& x2w, uint32_t& x3w) {
+  const uint32_t cbk = Tia::shade(byte_of(t.w0, 3), gray), c0 = Tia::shade(byte_of(t.w0, 0), gray),
+                 c1 = Tia::shade(byte_of(t.w0, 1), gray), cbl = Tia::shade(byte_of(t.w0, 2), gray);
+  const uint32_t ctrlpf = byte_of(t.w1, 3);
+  const uint32_t cp = (ctrlpf & 2u) ? (lane < 5u ? c0 : c1) : cbl;  // score mode: P0/P1 colour per half
+  const uint32_t hs = 16u * (lane & 1u);
+  const uint32_t q0 = (w.p0 | w.m0) >> hs, q1 = (w.p1 | w.m1) >> hs, qb = w.bl >> hs, qp = w.pf >> hs;
+  if (((q0 | q1 | qb) & 0xFFFFu) == 0u) {
+    x0w = cbk ^ ((cbk ^ cp) & nib_bytes(qp));
+    x1w = cbk ^ ((cbk ^ cp) & nib_bytes(qp >> 4));
+    x2w = cbk ^ ((cbk ^ cp) & nib_bytes(qp >> 8));
+    x3w = cbk ^ ((cbk ^ cp) & nib_bytes(qp >> 12));
+  } else {
+    const bool pfp = (ctrlpf & 4u) != 0u;
+    x0w = Tia::group_px(q0, q1, qb, qp, 0u, pfp, c0, c1, cbl, cp, cbk);
+    x1w = Tia::group_px(q0, q1, qb, qp, 4u, pfp, c0, c1, cbl, cp, cbk);
+    x2w = Tia::group_px(q0, q1, qb, qp, 8u, pfp, c0, c1, cbl, cp, cbk);
+    x3w = Tia::group_px(q0, q1, qb, qp, 12u, pfp, c0, c1, cbl, cp, cbk);
+  }
+}
+
+// store the completed row and start the next
+__device__ __forceinline__ void row_done(RowBuf& rb, uint32_t lane) {
+  if (lane < 10u) reinterpret_cast<uint4*>(rb.frame + rb.row * 160u)[lane] = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
+  rb.r0 = rb.r1 = rb.r2 = rb.r3 = rb.fill;
+  ++rb.row;
+}
+
+// advance the warp-uniform TIA over colour clocks [t.t, t_to)
+__device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb, uint32_t lane, uint32_t ystart,
+                                              const uint8_t* gray) {
+  const uint32_t t0 = t.t;
+  if (t_to <= t0) return;
+  t.t = t_to;
+  const uint32_t l0 = t0 / 228u, l1 = (t_to - 1) / 228u;
+  const uint32_t h0 = t0 - l0 * 228u, h1 = t_to - l1 * 228u;
+  const uint32_t xa0 = h0 > 68u ? h0 - 68u : 0u;
+  const uint32_t xb1 = h1 > 68u ? h1 - 68u : 0u;
+  const bool vblank = t.f(0) != 0u;
+  const bool need_coll = !vblank && t.open_pairs() != 0u;
+  const uint32_t w0 = ystart, w1 = ystart + (uint32_t)kFrameH;
+  const bool any_win = rb.render && l1 >= w0 && l0 < w1;
+  if (!need_coll && !any_win) return;
+  Words w{0u, 0u, 0u, 0u, 0u, 0u};
+  if (!vblank) w = object_words(t, lane < 10u ? (lane >> 1) : 0u);
+  if (need_coll) {  // collisions depend on x only: the union of the span's visible x ranges
+    uint32_t bits;
+    if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) {
+      bits = collide_coop(w, lane, 0u, 160u);
+    } else if (l1 == l0) {
+      bits = xb1 > xa0 ? collide_coop(w, lane, xa0, xb1) : 0u;
+    } else {
+      bits = (xa0 < 160u ? collide_coop(w, lane, xa0, 160u) : 0u) | (xb1 > 0u ? collide_coop(w, lane, 0u, xb1) : 0u);
+    }
+    t.w7 |= bits << 16;
+  }
+  if (!any_win) return;
+  uint32_t x0w = rb.fill, x1w = rb.fill, x2w = rb.fill, x3w = rb.fill;
+  if (!vblank && lane < 10u) chunk_px(t, w, lane, gray, x0w, x1w, x2w, x3w);
+  const int32_t comb = vblank ? -1 : t.comb_line();
+  const uint32_t la = l0 > w0 ? l0 : w0, lb = l1 < w1 - 1u ? l1 : w1 - 1u;
+  const uint32_t cx = 16u * lane;
+  for (uint32_t ln = la; ln <= lb; ++ln) {
+    const uint32_t xa = ln == l0 ? xa0 : 0u, xb = ln == l1 ? xb1 : 160u;
+    if (xb <= xa) continue;
+    if (lane < 10u && xa < cx + 16u && xb > cx) {
+      const bool cb = (int32_t)ln == comb && lane == 0u;  // HMOVE comb: x < 8 black (R#11)
+      const uint32_t p0 = cb ? rb.fill : x0w, p1 = cb ? rb.fill : x1w;
+      if (xa <= cx && xb >= cx + 16u) {
+        rb.r0 = p0; rb.r1 = p1; rb.r2 = x2w; rb.r3 = x3w;
+      } else {
+        const uint32_t m0 = group_mask(cx, xa, xb), m1 = group_mask(cx + 4u, xa, xb),
+                       m2 = group_mask(cx + 8u, xa, xb), m3 = group_mask(cx + 12u, xa, xb);
+        rb.r0 = (rb.r0 & ~m0) | (p0 & m0);
+        rb.r1 = (rb.r1 & ~m1) | (p1 & m1);
+        rb.r2 = (rb.r2 & ~m2) | (x2w & m2);
+        rb.r3 = (rb.r3 & ~m3) | (x3w & m3);
+      }
+    }
+    if (xb == 160u) row_done(rb, lane);
+  }
+}
+
+// replay n entries of the warp's log, then (optionally) advance to t_final; returns collisions
+__device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg, uint32_t n, bool fin,
+                                               uint32_t t_final, RowBuf& rb, uint32_t lane, uint32_t ystart,
+                                               const uint8_t* gray) {
+  TiaP t;
+  t.load(tw);
+  for (uint32_t k = 0; k < n; ++k) {
+    const uint32_t e = lg[k];
+    const uint32_t T = e >> 14;
+    catch_up_coop(t, T, rb, lane, ystart, gray);
+    t.apply((e >> 8) & 0x3Fu, e & 0xFFu, T);
+  }
+  if (fin) catch_up_coop(t, t_final, rb, lane, ystart, gray);
+  __syncwarp();
+  if (lane == 0u) t.store(tw);
+  __syncwarp();
+  return t.coll();
+}
+
+// after the frame's last catch-up: store the partial row and black out the rows never reached
+__device__ __forceinline__ void finish_frame_coop(RowBuf& rb, uint32_t lane) {
+  if (!rb.render) return;
+  if (rb.row < (uint32_t)kFrameH) {
+    if (lane < 10u) reinterpret_cast<uint4*>(rb.frame + rb.row * 160u)[lane] = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
+    const uint32_t first = (rb.row + 1u) * 10u;
+    uint4* p = reinterpret_cast<uint4*>(rb.frame);
+    for (uint32_t q = first + lane; q < (uint32_t)kFrameChunks; q += 32u) p[q] = make_uint4(rb.fill, rb.fill, rb.fill, rb.fill);
+  }
+  rb.render = false;
+}
+
+}  // namespace cule

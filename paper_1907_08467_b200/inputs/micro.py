@@ -570,3 +570,100 @@ Data: .byte {f(vals[0:16])}
 MulA: .byte {f(vals[16:32])}
 MulB: .byte {f(vals[32:48])}
 """ + _VECTORS
+
+
+# ---------------------------------------------------------------------------------------------
+# M20 timer polls: the RIOT polling idioms of Atari kernels (timer read + branch back), with
+# timer values that vary per frame and per action, a loop whose branch crosses a page, and
+# time-sensitive reads right after each loop (RAM $81-$85).  M21: a TIMINT poll that never
+# exits (runaway at the line cap).  Used for engine-vs-oracle parity.
+# ---------------------------------------------------------------------------------------------
+def m20_timer_polls() -> str:
+    return _HEAD + """
+Frame:
+    LDA #2
+    STA WSYNC
+    STA VSYNC
+    STA WSYNC
+    STA WSYNC
+    STA WSYNC
+    LDA #0
+    STA VSYNC
+    INC $80
+    LDA $80
+    AND #$1F
+    ORA #1
+    STA TIM8T
+P1: LDA INTIM
+    BNE P1
+    LDA INTIM
+    STA $81
+    LDA $80
+    AND #7
+    STA TIM64T
+P2: BIT TIMINT
+    BPL P2
+    LDA INTIM
+    STA $82
+    LDA #3
+    STA T1024T
+    LDA SWCHA
+    AND #3
+P3: CMP INTIM
+    BNE P3
+    LDX INTIM
+    STX $83
+    LDA $80
+    STA TIM1T
+P4: LDX INTIM
+    BPL P4
+    STX $84
+    JMP Cross
+    .org $F2FC
+Cross:
+    LDA #20
+    STA TIM8T
+P5: LDA INTIM
+    BNE P5
+    LDA INTIM
+    STA $85
+    LDX #150
+L1: STA WSYNC
+    DEX
+    BNE L1
+    JMP Frame
+""" + _VECTORS
+
+
+def m21_timint_spin(after_frames: int = 3) -> str:
+    return _HEAD + f"""
+    LDA #0
+    STA $80
+Frame:
+    LDA #2
+    STA WSYNC
+    STA VSYNC
+    LDA #0
+    STA VSYNC
+    INC $80
+    LDA $80
+    CMP #{after_frames + 2}
+    BNE Ok
+    LDA #9
+    STA TIM8T
+W:  BIT TIMINT
+    BPL W
+Spin:
+    BIT TIMINT
+    BMI Spin
+Ok:
+    LDA #40
+    STA TIM64T
+W2: LDA INTIM
+    BNE W2
+    LDX #200
+L2: STA WSYNC
+    DEX
+    BNE L2
+    JMP Frame
+""" + _VECTORS

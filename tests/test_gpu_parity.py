@@ -14,6 +14,14 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+@pytest.fixture(autouse=True, params=["simt", "scalar"])
+def engine(request, monkeypatch):
+    """Every parity test runs on both engines: the batched SIMT datapath and the scalar engine
+    (one env per warp, compact interpreter, warp-cooperative TIA replay)."""
+    monkeypatch.setenv("CULE_ENGINE", request.param)
+    return request.param
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _built():
     if not torch.cuda.is_available():
@@ -110,7 +118,8 @@ def test_episode_ends_and_resets():
     assert n_done > 96
 
 
-@pytest.mark.parametrize("src", [micro.m17_score(), micro.m14_jam(100), micro.m15_no_vsync(100)])
+@pytest.mark.parametrize("src", [micro.m17_score(), micro.m14_jam(100), micro.m15_no_vsync(100),
+                                 micro.m20_timer_polls(), micro.m21_timint_spin(100)])
 def test_micro_programs_env(src):
     rom = micro.build(src)
     gpu, ref = pair([rom, games.build_rom("R1")], 34, 4, reset_cache_size=3, max_random_frames=2)
