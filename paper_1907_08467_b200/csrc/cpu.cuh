@@ -49,6 +49,9 @@ struct Cpu {
   uint32_t tV, tS, swcha, inpt4;
   int32_t tW;
   uint32_t vsync, log_len, fault;
+  // idle-loop skip (exact): timer-read constancy (cycles) of this instruction's data read, and
+  // the previous instruction when it was a plain timer read (its PC and cycles)
+  uint32_t ff, ppc, pn, pff;
 
   __device__ __forceinline__ uint32_t getP() const {
     return (nreg & 0x80u) | (V << 6) | 0x20u | (D << 3) | (I << 2) | ((zreg & 0xFFu) == 0 ? 2u : 0u) | C;
@@ -73,6 +76,22 @@ struct Cpu {
     int32_t VI = (int32_t)(tV << tS);
     if (a & 1u) return e > VI ? 0x80u : 0u;
     if (e <= VI) return (tV - (uint32_t)((e + (1 << tS) - 1) >> tS)) & 0xFFu;
+    return (uint32_t)(0xFF - (e - VI - 1)) & 0xFFu;
+  }
+  // the same read, also noting for how many more cycles the value read stays the same
+  __device__ __forceinline__ uint32_t riot_read_ff(uint32_t a) {
+    if (!(a & 0x04u)) return riot_read(a);
+    const int32_t e = (int32_t)now - tW;
+    const int32_t VI = (int32_t)(tV << tS);
+    if (a & 1u) {
+      ff = e > VI ? 0x7FFFFFFFu : (uint32_t)(VI - e);
+      return e > VI ? 0x80u : 0u;
+    }
+    if (e <= VI) {
+      const int32_t q = (e + (1 << tS) - 1) >> tS;
+      ff = (uint32_t)((q << tS) - e);
+      return (tV - (uint32_t)q) & 0xFFu;
+    }
     return (uint32_t)(0xFF - (e - VI - 1)) & 0xFFu;
   }
 
@@ -100,7 +119,7 @@ struct Cpu {
       if (r < 8u) return tia_coll_read(c, r, kPhaseA ? t_phaseA : 3u * now);
       return r == 0x0Cu ? inpt4 : (r == 0x0Du ? 0x80u : 0u);
     }
-    return riot_read(a);
+    return kPhaseA ? riot_read(a) : riot_read_ff(a);
   }
 
   __device__ __forceinline__ void wr(const Ctx& c, uint32_t addr, uint32_t v) {
@@ -136,6 +155,7 @@ struct Cpu {
   __device__ __forceinline__ uint32_t pull(const Ctx& c) { SP = (SP + 1) & 0xFFu; return rd<false>(c, 0x100u | SP); }
 
   // ---- one instruction; returns an Event ------------------------------------------------------
+  template <bool kSkip>
   __device__ __forceinline__ uint32_t exec(const Ctx& c) {
     now = fc;
     wsync_pending = 0;
@@ -179,11 +199,20 @@ struct Cpu {
       const uint32_t tgt = (PC + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
       n += taken ? 1u + (((tgt ^ PC) >> 8) & 1u) : 0u;
       PC = taken ? tgt : PC;
+      // idle-loop skip: [plain timer read; branch back to it] — the iterations whose read falls
+      // in the same constant interval repeat this one exactly, so only time advances (stopping
+      // short of the runaway cap, which the loop then reaches normally).  Same rule as the
+      // scalar engine (scalar_cpu.cuh).
+      if (kSkip && taken && pff != 0u && tgt == ppc && (pc & 0x1000u) && fc + n < c.cap_cycles) {
+        const uint32_t P = pn + n;
+        n += min(pff / P, (c.cap_cycles - 1u - (fc + n)) / P) * P;
+      }
     }
     if (lo & dk::JMP) PC = ea;
 
     // ---- phase C ---------------------------------------------------------------------------------
     now = fc + n;
+    ff = 0u;
     uint32_t v = b1;  // immediate operand
     if (lo & dk::RD) v = rd<false>(c, ea);
 
@@ -229,6 +258,13 @@ struct Cpu {
     if (spc) special(c, spc, v, ea);
 
     // ---- end of instruction ------------------------------------------------------------------------
+    // a plain timer read (cartridge code, abs, read-only, idempotent effect) can head an idle loop
+    const bool plain = (pc & 0x1000u) && (lo & dk::RD) && !(lo & dk::WR) && spc == 0u &&
+                       !(lo & (dk::ZP | dk::ZIX | dk::ZIY | dk::AIX | dk::AIY | dk::PTRZ | dk::PTRA)) &&
+                       !(hi & (dk::LOGIC | dk::ADDV));
+    pff = plain ? ff : 0u;
+    ppc = pc;
+    pn = now - fc;
     fc = now;
     t_phaseA = 3u * now;
     if (wsync_pending) fc = ((fc + 75u) / 76u) * 76u;  // stall to the next line start (R#5)

@@ -172,6 +172,9 @@ __device__ __forceinline__ void load_machine(Cpu& m, const Ctx& c, const Hdr& h,
   m.log_len = 0;
   m.t_phaseA = 3u * m.fc;
   m.now = m.fc;
+  m.pff = 0u;
+  m.ppc = 0xFFFFFFFFu;
+  m.pn = 0u;
   // TIA words (tia.cuh Tia::load layout)
   const uint32_t s = c.s;
   uint32_t* w = c.tw;
@@ -290,7 +293,7 @@ __device__ __forceinline__ int32_t simulate(Cpu& m, const Ctx& c, bool active, u
       if (kDebug && count >= budget) {
         ev = EV_BUDGET;
       } else {
-        ev = m.exec(c);
+        ev = m.template exec<!kDebug>(c);
         ++count;
       }
     }
