@@ -54,7 +54,7 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   L->cstage = take(gray ? 2 * nk * cule::kFrameBytes : 0);
   L->roms = take(4 * 8192);
   L->decode = take(2048);
-  L->sdecode = take(1024);
+  L->sdecode = take(2048);
   L->gray = take(128);
   L->counters = take(32);
   L->err = take(16);
@@ -98,7 +98,7 @@ static cule::Params base_params(const cule_env* e) {
   p.f8_mask = e->f8_mask;
   p.n_roms = (uint32_t)e->n_roms;
   p.decode = reinterpret_cast<const uint64_t*>(e->ws + e->L.decode);
-  p.sdecode = reinterpret_cast<const uint32_t*>(e->ws + e->L.sdecode);
+  p.sdecode = reinterpret_cast<const uint64_t*>(e->ws + e->L.sdecode);
   p.gray = e->ws + e->L.gray;
   p.cache_state = e->ws + e->L.cstate;
   p.cache_score = reinterpret_cast<const uint16_t*>(e->ws + e->L.cscore);
@@ -289,7 +289,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   for (int r = 0; r < n_roms; ++r) std::memcpy(romimg + e->rom_off[r], roms[r], rom_lens[r]);
   uint64_t table[256];
   cule::build_decode_table(table);
-  uint32_t stable[256];
+  uint64_t stable[256];
   cule::build_scalar_table(stable);
   uint8_t gray[128] = {0};
   if (cfg->palette_rgb) {

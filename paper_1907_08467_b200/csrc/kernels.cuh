@@ -40,7 +40,7 @@ struct Params {
   uint32_t f8_mask;
   uint32_t n_roms;
   const uint64_t* decode;    // [256] batched-engine decode table
-  const uint32_t* sdecode;   // [256] scalar-engine decode table
+  const uint64_t* sdecode;   // [256] scalar-engine decode table
   const uint8_t* gray;       // [128]
   const uint8_t* cache_state;// [n_roms*K][256] packed
   const uint16_t* cache_score;

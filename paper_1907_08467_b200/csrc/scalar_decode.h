@@ -1,5 +1,5 @@
 // scalar_decode.h — host-side construction of the decode table of the scalar engine
-// (one 32-bit entry per opcode, staged into shared memory once per block).
+// (one 64-bit entry per opcode, staged into shared memory once per block).
 //
 // The scalar engine runs one env per warp, so an instruction pays only for its own work.  Its
 // entry therefore names an operation ("kind", one case of a small jump table) and carries the
@@ -7,7 +7,8 @@
 // and only the pointer modes branch.  Kinds that differ only in a register (LDA/LDX/LDY/LAX,
 // STA/STX/STY/SAX, CMP/CPX/CPY, INX/INY/DEX/DEY, the transfers, flag set/clear, the eight
 // branches) share one case and read that register from the AUX field, which keeps the jump
-// table — and the instruction-cache footprint of the hot loop — small.
+// table — and the instruction-cache footprint of the hot loop — small.  The index operand of
+// indexed modes comes from a byte-permute selector stored in the entry (one instruction).
 // Cycle counts come from the same addressing-mode x access-class rules as decode_table.h
 // (SURVEY.md Appendix A), not from a per-opcode list.
 #pragma once
@@ -21,28 +22,29 @@
 namespace cule {
 
 namespace sk {
-constexpr uint32_t LEN = 0;         // 2 bits: instruction length 1..3
-constexpr uint32_t CYC = 2;         // 4 bits: base cycles
-constexpr uint32_t PEN = 1u << 6;   // +1 cycle on a page cross (reads through abs,X / abs,Y / (zp),Y)
-constexpr uint32_t RD = 1u << 7;    // data read at EA (phase C)
-constexpr uint32_t WR = 1u << 8;    // data write at EA (phase C)
-constexpr uint32_t ZP = 1u << 9;    // EA = zero-page address
-constexpr uint32_t ZIX = 1u << 10;  // zero-page index X (zp,X and (zp,X))
-constexpr uint32_t ZIY = 1u << 11;  // zero-page index Y (zp,Y)
-constexpr uint32_t AIX = 1u << 12;  // 16-bit index X (abs,X)
-constexpr uint32_t AIY = 1u << 13;  // 16-bit index Y (abs,Y and (zp),Y)
-constexpr uint32_t PTRZ = 1u << 14; // pointer read from zero page
-constexpr uint32_t PTRA = 1u << 15; // pointer read with the page-wrap bug (JMP (abs))
-constexpr uint32_t ACC = 1u << 16;  // operand = A and result -> A (accumulator shifts)
-constexpr uint32_t AUX = 17;        // 7 bits, kind-specific
-constexpr uint32_t KIND = 24;       // 8 bits
+// low word: bits 0-15 = byte selector for the index operand: __byte_perm(X | Y << 8, 0, lo)
+// yields X, Y or 0 in one instruction (no selects); then single-bit flags
+constexpr uint32_t SEL_NONE = 0x4444, SEL_X = 0x4440, SEL_Y = 0x4441;
+constexpr uint32_t LEN = 16;        // 2 bits: instruction length 1..3
+constexpr uint32_t CYC = 18;        // 4 bits: base cycles
+constexpr uint32_t PEN = 1u << 22;  // +1 cycle on a page cross (reads through abs,X / abs,Y / (zp),Y)
+constexpr uint32_t RD = 1u << 23;   // data read at EA (phase C)
+constexpr uint32_t WR = 1u << 24;   // data write at EA (phase C)
+constexpr uint32_t ZP = 1u << 25;   // zero page: EA (or, with PTRZ, the pointer address) wraps at 8 bits
+constexpr uint32_t PTRZ = 1u << 26; // pointer read from zero page ((zp,X): index before, (zp),Y: after)
+constexpr uint32_t PTRA = 1u << 27; // pointer read with the page-wrap bug (JMP (abs))
+constexpr uint32_t ACC = 1u << 28;  // operand = A (accumulator shifts)
+constexpr uint32_t PLAIN = 1u << 29;// plain absolute read of an idempotent kind (idle-loop head)
+// high word
+constexpr uint32_t KIND = 0;        // 8 bits
+constexpr uint32_t AUX = 8;         // 7 bits, kind-specific
 }  // namespace sk
 
 enum Kind : uint32_t {
   K_JAM = 0, K_NOP, K_ORA, K_AND, K_EOR, K_ADC, K_SBC, K_CMP, K_BIT, K_LD, K_ST,
   K_ASL, K_LSR, K_ROL, K_ROR, K_INC, K_DEC, K_SLO, K_RLA, K_SRE, K_RRA, K_DCP, K_ISB,
   K_INR, K_TR, K_FLAG, K_BR, K_JMP, K_JSR, K_RTS, K_RTI, K_BRK, K_PHA, K_PHP, K_PLA, K_PLP,
-  K_ANC, K_ALR, K_ARR, K_SBX, K_COUNT
+  K_ANC, K_ALR, K_ARR, K_SBX, K_ASLA, K_LSRA, K_ROLA, K_RORA, K_COUNT
 };
 // AUX encodings
 //   K_CMP: register 0 A, 1 X, 2 Y          K_LD: destination bits 1 A, 2 X, 4 Y
@@ -53,29 +55,30 @@ enum Kind : uint32_t {
 
 inline uint32_t s_mode_bits(uint32_t mode) {
   switch (mode) {
-    case AM_ZP: return sk::ZP;
-    case AM_ZPX: return sk::ZP | sk::ZIX;
-    case AM_ZPY: return sk::ZP | sk::ZIY;
-    case AM_ABSX: return sk::AIX;
-    case AM_ABSY: return sk::AIY;
-    case AM_IND: return sk::PTRA;
-    case AM_INDX: return sk::PTRZ | sk::ZIX;
-    case AM_INDY: return sk::PTRZ | sk::AIY;
-    default: return 0;
+    case AM_ZP: return sk::ZP | sk::SEL_NONE;
+    case AM_ZPX: return sk::ZP | sk::SEL_X;
+    case AM_ZPY: return sk::ZP | sk::SEL_Y;
+    case AM_ABSX: return sk::SEL_X;
+    case AM_ABSY: return sk::SEL_Y;
+    case AM_IND: return sk::PTRA | sk::SEL_NONE;
+    case AM_INDX: return sk::PTRZ | sk::ZP | sk::SEL_X;
+    case AM_INDY: return sk::PTRZ | sk::SEL_Y;
+    default: return sk::SEL_NONE;
   }
 }
 
-inline uint32_t s_entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr, uint32_t kind, uint32_t aux) {
-  uint32_t e = s_mode_bits(mode) | (mode_len(mode) << sk::LEN) | (cyc << sk::CYC) | (aux << sk::AUX) |
-               (kind << sk::KIND);
-  if (pen) e |= sk::PEN;
-  if (rd) e |= sk::RD;
-  if (wr) e |= sk::WR;
-  if (mode == AM_ACC) e |= sk::ACC;
-  return e;
+inline uint64_t s_entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr, uint32_t kind, uint32_t aux) {
+  uint32_t lo = s_mode_bits(mode) | (mode_len(mode) << sk::LEN) | (cyc << sk::CYC);
+  if (pen) lo |= sk::PEN;
+  if (rd) lo |= sk::RD;
+  if (wr) lo |= sk::WR;
+  if (mode == AM_ACC) lo |= sk::ACC;
+  if (mode == AM_ABS && rd && !wr && (kind == K_LD || kind == K_BIT || kind == K_CMP || kind == K_NOP)) lo |= sk::PLAIN;
+  const uint32_t hi = (kind << sk::KIND) | (aux << sk::AUX);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
-inline void build_scalar_table(uint32_t* t) {
+inline void build_scalar_table(uint64_t* t) {
   // JAM and the unstable opcodes: 1-byte fetch, 0 cycles, fault (DESIGN.md §2 R#1)
   for (int i = 0; i < 256; i++) t[i] = s_entry(AM_IMP, 0, false, false, false, K_JAM, 0);
   auto group = [&](uint32_t kind, uint32_t aux, AccessClass cl,
@@ -115,7 +118,8 @@ inline void build_scalar_table(uint32_t* t) {
   for (auto& g : rmw) {
     const uint32_t b = g[1];
     group(g[0], 0, CL_RMW, {{AM_ZP, b + 0x06}, {AM_ABS, b + 0x0E}, {AM_ZPX, b + 0x16}, {AM_ABSX, b + 0x1E}});
-    if (g[0] != K_DEC && g[0] != K_INC) t[b + 0x0A] = s_entry(AM_ACC, 2, false, false, false, g[0], 0);
+    if (g[0] != K_DEC && g[0] != K_INC)
+      t[b + 0x0A] = s_entry(AM_ACC, 2, false, false, false, g[0] - K_ASL + K_ASLA, 0);
   }
   const uint32_t urmw[6][2] = {{K_SLO, 0x00}, {K_RLA, 0x20}, {K_SRE, 0x40}, {K_RRA, 0x60}, {K_DCP, 0xC0}, {K_ISB, 0xE0}};
   for (auto& g : urmw) {

@@ -23,10 +23,11 @@ constexpr uint32_t kSLogCap = 128;
 constexpr uint32_t kSOffTia = 128, kSOffMach = 176, kSOffStg = 304, kSOffLog = 384;
 constexpr uint32_t kSWarpBytes = kSOffLog + 4 * kSLogCap;
 constexpr uint32_t kSWarps = 4;  // warps (envs) per block
-constexpr uint32_t kSmSDecode = kSmRom;  // scalar decode table [256] u32 right after the gray LUT
+constexpr uint32_t kSmSDecode = kSmRom;  // scalar decode table [256] u64 right after the gray LUT
+constexpr uint32_t kSDecBytes = 2048;
 
 __host__ __device__ __forceinline__ size_t scalar_smem_bytes(uint32_t rom_bytes) {
-  return kSmSDecode + 1024u + rom_bytes + (size_t)kSWarps * kSWarpBytes;
+  return kSmSDecode + kSDecBytes + rom_bytes + (size_t)kSWarps * kSWarpBytes;
 }
 
 __device__ __forceinline__ bool env_of_slot(const Params& p, uint32_t s, uint32_t& i) {
@@ -124,7 +125,7 @@ __device__ __forceinline__ void end_frame_s(SMach* M, uint32_t* tw) {
 
 // one env for one step (or one debug budget); all 32 lanes of the warp call it together
 template <bool kGray, bool kDebug>
-__device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, const uint32_t* dtab, uint8_t* ram,
+__device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, const uint64_t* dtab, uint8_t* ram,
                                               uint32_t* lg, uint32_t* tw, uint32_t cap_cycles, uint32_t lane,
                                               uint32_t nframes, uint8_t* frame_out, uint32_t& episode_frames,
                                               int32_t budget, uint32_t ystart, const uint8_t* gray) {
@@ -189,12 +190,12 @@ __device__ __forceinline__ void stage_block_s(const Params& p, uint8_t* smem) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, 1024u + 128u + p.rom_bytes);
-    bulk_g2s(smem + kSmSDecode, p.sdecode, 1024u, bar);
+    mbar_expect_tx(bar, kSDecBytes + 128u + p.rom_bytes);
+    bulk_g2s(smem + kSmSDecode, p.sdecode, kSDecBytes, bar);
     bulk_g2s(smem + kSmGray, p.gray, 128u, bar);
     for (uint32_t r = 0; r < p.n_roms; ++r) {
       const uint32_t len = ((p.f8_mask >> r) & 1u) ? 8192u : 4096u;
-      bulk_g2s(smem + kSmSDecode + 1024u + p.rom_off[r], p.roms + p.rom_off[r], len, bar);
+      bulk_g2s(smem + kSmSDecode + kSDecBytes + p.rom_off[r], p.roms + p.rom_off[r], len, bar);
     }
   }
   __syncthreads();
@@ -206,9 +207,9 @@ __global__ void __launch_bounds__(32 * kSWarps, CULE_SMINB) scalar_kernel(Params
   extern __shared__ __align__(16) uint8_t smem[];
   stage_block_s(p, smem);
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
-  const uint8_t* rom_all = smem + kSmSDecode + 1024u;
-  const uint32_t* dtab = reinterpret_cast<const uint32_t*>(smem + kSmSDecode);
-  uint8_t* wb = smem + kSmSDecode + 1024u + p.rom_bytes + wib * kSWarpBytes;
+  const uint8_t* rom_all = smem + kSmSDecode + kSDecBytes;
+  const uint64_t* dtab = reinterpret_cast<const uint64_t*>(smem + kSmSDecode);
+  uint8_t* wb = smem + kSmSDecode + kSDecBytes + p.rom_bytes + wib * kSWarpBytes;
   uint8_t* ram = wb;
   uint32_t* tw = reinterpret_cast<uint32_t*>(wb + kSOffTia);
   SMach* M = reinterpret_cast<SMach*>(wb + kSOffMach);
