@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-envs", type=int, default=16)
     ap.add_argument("--cpu-sample-steps", type=int, default=100)
+    ap.add_argument("--idle-skip", type=int, default=0, choices=[0, 1],
+                    help="exact idle-loop skip (off for the headline, SURVEY.md §7c.8)")
+    ap.add_argument("--no-variant", action="store_true", help="skip the idle-skip-on variant run")
     return ap.parse_args()
 
 
@@ -219,7 +222,7 @@ def run_cule(args, rank, world, local_rank):
         envs = args.envs
     roms = [games.build_rom(n) for n in rom_names]
     base, _ = D.shard(envs, rank)
-    env = Env(roms, envs, fs, obs_mode=mode, env_index_base=base, device=dev)
+    env = Env(roms, envs, fs, obs_mode=mode, env_index_base=base, device=dev, idle_skip=args.idle_skip)
     stream = torch.cuda.current_stream(dev)
     env.reset(0)
     gen = torch.Generator(device=dev)

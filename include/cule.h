@@ -64,7 +64,8 @@ typedef struct {
   uint8_t score_addr;         /* RAM bus address ($80-$FE) of the BCD score high byte; low at +1 */
   uint8_t term_addr;          /* done iff (RAM[term_addr] & term_mask) != 0 ($80-$FF)        */
   uint8_t term_mask;
-  uint8_t reserved_;
+  uint8_t idle_skip;          /* 1: exact closed-form skip of [timer read; branch back] poll loops
+                                 (results bit-identical), 0 (default): off   */
   uint64_t seed;              /* reset-cache construction seed (u_k draws)                   */
   int64_t env_index_base;     /* global id of local env 0 (multi-GPU sharding)               */
   const uint8_t* palette_rgb; /* HOST, 128 x (R,G,B) NTSC palette; read only during

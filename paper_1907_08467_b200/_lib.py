@@ -35,7 +35,7 @@ class CuleConfig(ctypes.Structure):
                 ("max_episode_frames", ctypes.c_int32), ("line_cap", ctypes.c_int32),
                 ("ystart", ctypes.c_int32), ("score_addr", ctypes.c_uint8),
                 ("term_addr", ctypes.c_uint8), ("term_mask", ctypes.c_uint8),
-                ("reserved_", ctypes.c_uint8), ("seed", ctypes.c_uint64),
+                ("idle_skip", ctypes.c_uint8), ("seed", ctypes.c_uint64),
                 ("env_index_base", ctypes.c_int64),
                 ("palette_rgb", ctypes.POINTER(ctypes.c_uint8))]
 

@@ -40,6 +40,7 @@ struct Ctx {
   uint32_t s;             // word stride = blockDim
   uint32_t ystart, line_cap;
   uint32_t cap_cycles;    // 76 * line_cap
+  uint32_t idle_skip;     // exact idle-loop skip enabled (cule_config.idle_skip)
 };
 
 struct Cpu {
@@ -262,7 +263,7 @@ struct Cpu {
     const bool plain = (pc & 0x1000u) && (lo & dk::RD) && !(lo & dk::WR) && spc == 0u &&
                        !(lo & (dk::ZP | dk::ZIX | dk::ZIY | dk::AIX | dk::AIY | dk::PTRZ | dk::PTRA)) &&
                        !(hi & (dk::LOGIC | dk::ADDV));
-    pff = plain ? ff : 0u;
+    pff = (plain && c.idle_skip) ? ff : 0u;
     ppc = pc;
     pn = now - fc;
     fc = now;

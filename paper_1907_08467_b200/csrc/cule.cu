@@ -122,6 +122,7 @@ static cule::Params base_params(const cule_env* e) {
   p.cache_staging = e->ws + e->L.cstage;
   p.error_flag = reinterpret_cast<int32_t*>(e->ws + e->L.err);
   p.epw = e->epw;
+  p.idle_skip = e->cfg.idle_skip ? 1u : 0u;
   for (int r = 0; r < 4; ++r) { p.slot_start[r] = e->slot_start[r]; p.first_env[r] = e->first_env[r]; }
   return p;
 }
@@ -204,6 +205,7 @@ void cule_default_config(cule_config* c) {
   c->term_mask = 0x01;
   c->seed = 0;
   c->env_index_base = 0;
+  c->idle_skip = 0;
   c->palette_rgb = nullptr;
 }
 

@@ -62,6 +62,7 @@ struct Params {
   uint32_t epw;
   uint32_t slot_start[4];   // first slot of ROM r
   uint32_t first_env[4];    // first local env of ROM r (envs of ROM r are first_env[r] + n_roms*k)
+  uint32_t idle_skip;       // exact idle-loop skip (cule_config.idle_skip; off by default)
 };
 
 // The env a thread emulates.  Envs are laid out so that the lanes of a warp run the same ROM
@@ -142,6 +143,7 @@ __device__ __forceinline__ Ctx stage_block(const Params& p, uint8_t* smem, bool 
   c.ystart = p.ystart;
   c.line_cap = p.line_cap;
   c.cap_cycles = 76u * p.line_cap;
+  c.idle_skip = p.idle_skip;
   return c;
 }
 

@@ -39,7 +39,8 @@ struct SMach {
   uint32_t tia_done;  // the TIA has been replayed to this colour clock
   uint32_t pa_T, pa_coll;  // latches kept for a phase-A read at pa_T (see run_cpu)
   uint32_t abort_T, abort_pa;
-  uint32_t pad0, pad1;
+  uint32_t idle_skip;  // exact idle-loop skip enabled (cule_config.idle_skip)
+  uint32_t pad1;
 };
 static_assert(sizeof(SMach) == 32 * 4, "SMach is 32 words");
 
@@ -163,6 +164,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   uint32_t ev = SE_NONE;
   // idle-loop skip (exact): the previous instruction, if it was a plain timer read
   uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u;
+  const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
   for (;;) {
     if (kDebug && budget <= 0) { ev = SE_BUDGET; break; }
     const uint32_t pc0 = PC, bank0 = bank;
@@ -447,7 +449,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       if (d & sk::WR) wr(ea, wv);
       if (kDebug) --budget;
       // idle-loop head candidate: plain timer read in cartridge code
-      pff = (d & sk::PLAIN) ? ff : 0u;
+      pff = (d & sk::PLAIN) ? (ff & skip_mask) : 0u;
       ppc = pc0;
       pn = n;
       // ---- end of instruction (R#4, R#5) --------------------------------------------------

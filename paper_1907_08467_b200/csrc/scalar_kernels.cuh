@@ -59,6 +59,7 @@ __device__ __forceinline__ void load_smach(SMach* M, const Hdr& h, const Params&
   M->tia_done = 3u * M->fc;
   M->coll = hw(h, 5) & 0xFFFFu;
   M->pa_T = 0xFFFFFFFFu;
+  M->idle_skip = p.idle_skip;
   tw[0] = hw(h, 7);
   tw[1] = pk(hb(h, 35), hb(h, 36), hb(h, 37), hb(h, 32));
   tw[2] = pk(hb(h, 26), hb(h, 27), hb(h, 38), hb(h, 39));
