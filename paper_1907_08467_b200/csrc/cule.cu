@@ -14,7 +14,10 @@
 #include "../../include/cule.h"
 #include "decode_table.h"
 #include "kernels.cuh"
+#include <vector>
+
 #include "scalar_decode.h"
+#include "scalar_predecode.h"
 #include "scalar_kernels.cuh"
 
 namespace {
@@ -31,8 +34,8 @@ int fail(int code, const std::string& msg) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t state, pack, staging, cstate, cobs, cscore, cstage, roms, decode, sdecode, gray, counters, err,
-      io_act, io_obs, io_rew, io_done, total;
+  size_t state, pack, staging, cstate, cobs, cscore, cstage, roms, decode, sdecode, srec, gray, counters, err,
+      tickets, io_act, io_obs, io_rew, io_done, total;
 };
 
 size_t obs_bytes_of(int mode) { return mode == CULE_OBS_RAW ? (size_t)cule::kFrameBytes : (size_t)cule::kObs84; }
@@ -55,9 +58,11 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   L->roms = take(4 * 8192);
   L->decode = take(2048);
   L->sdecode = take(2048);
+  L->srec = take(cule::kRecBytes * 4 * 8192);
   L->gray = take(128);
   L->counters = take(32);
   L->err = take(16);
+  L->tickets = take(16);
   L->io_act = take(n);
   L->io_obs = take(n * ob);
   L->io_rew = take(4 * n);
@@ -82,6 +87,8 @@ struct cule_env {
   uint32_t epw;            // envs per warp
   int engine;              // 0 batched (SIMT datapath, epw envs per warp), 1 scalar (one env per warp)
   size_t ssmem;            // dynamic shared memory of the scalar kernels
+  uint32_t use_rec;        // scalar engine: pre-decoded records fit in shared memory
+  uint32_t sgrid;          // scalar engine: persistent blocks (<= one per SM)
   uint32_t slot_start[4], first_env[4];
   uint32_t grid;           // blocks of the step / debug kernels
 };
@@ -123,6 +130,9 @@ static cule::Params base_params(const cule_env* e) {
   p.error_flag = reinterpret_cast<int32_t*>(e->ws + e->L.err);
   p.epw = e->epw;
   p.idle_skip = e->cfg.idle_skip ? 1u : 0u;
+  p.srec = reinterpret_cast<const uint64_t*>(e->ws + e->L.srec);
+  p.use_rec = e->use_rec;
+  p.tickets = reinterpret_cast<unsigned int*>(e->ws + e->L.tickets);
   for (int r = 0; r < 4; ++r) { p.slot_start[r] = e->slot_start[r]; p.first_env[r] = e->first_env[r]; }
   return p;
 }
@@ -267,7 +277,20 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   e->rom_bytes = off;
   e->epw = choose_epw(num_envs);
   e->engine = choose_engine(num_envs);
-  e->ssmem = cule::scalar_smem_bytes(e->rom_bytes);
+  {
+    // records cost 8 B per ROM byte of shared memory: staged whenever they fit (all 4 KB and
+    // F8 combinations up to 4 x 4 KB / 2 x F8 + 1 x 4 KB); CULE_NO_REC=1 disables them
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (optin <= 0) optin = 232448;
+    const char* nr = getenv("CULE_NO_REC");
+    e->use_rec = (!(nr && atoi(nr) == 1) && cule::scalar_smem_bytes(e->rom_bytes, true) <= (size_t)optin) ? 1u : 0u;
+    e->ssmem = cule::scalar_smem_bytes(e->rom_bytes, e->use_rec != 0u);
+    const uint32_t need = ((uint32_t)num_envs + cule::kSWarps - 1) / cule::kSWarps;
+    const uint32_t sms = (uint32_t)sm_count();
+    e->sgrid = need < sms ? need : sms;
+  }
   {
     const uint32_t warps = ((uint32_t)num_envs + e->epw - 1) / e->epw;
     e->block = choose_block(warps);
@@ -293,6 +316,12 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   cule::build_decode_table(table);
   uint64_t stable[256];
   cule::build_scalar_table(stable);
+  std::vector<uint64_t> recs((size_t)e->rom_bytes);
+  {
+    uint32_t lens[4] = {0, 0, 0, 0};
+    for (int r = 0; r < n_roms; ++r) lens[r] = (uint32_t)rom_lens[r];
+    cule::predecode_roms(romimg, e->rom_off, lens, n_roms, recs.data());
+  }
   uint8_t gray[128] = {0};
   if (cfg->palette_rgb) {
     for (int i = 0; i < 128; ++i) {
@@ -303,6 +332,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   cudaMemcpy(e->ws + L.roms, romimg, e->rom_bytes, cudaMemcpyHostToDevice);
   cudaMemcpy(e->ws + L.decode, table, sizeof table, cudaMemcpyHostToDevice);
   cudaMemcpy(e->ws + L.sdecode, stable, sizeof stable, cudaMemcpyHostToDevice);
+  cudaMemcpy(e->ws + L.srec, recs.data(), recs.size() * sizeof(uint64_t), cudaMemcpyHostToDevice);
+  cudaMemset(e->ws + L.tickets, 0, 16);
   cudaMemcpy(e->ws + L.gray, gray, sizeof gray, cudaMemcpyHostToDevice);
   cudaMemset(e->ws + L.state, 0, 256 * (size_t)num_envs);
   cudaMemset(e->ws + L.counters, 0, 32);
@@ -368,7 +399,7 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
   p.rewards = d_rewards;
   p.dones = d_dones;
   if (e->engine == 1) {
-    const uint32_t sg = ((uint32_t)e->N + cule::kSWarps - 1) / cule::kSWarps;
+    const uint32_t sg = e->sgrid;
     if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::scalar_kernel<true, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
     else cule::scalar_kernel<false, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
   } else if (e->cfg.obs_mode == CULE_OBS_GRAY84) {
@@ -443,7 +474,7 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
   p.debug_instr = n_instr;
   p.debug_status = d_status;
   if (e->engine == 1) {
-    const uint32_t sg = ((uint32_t)e->N + cule::kSWarps - 1) / cule::kSWarps;
+    const uint32_t sg = e->sgrid;
     cule::scalar_kernel<false, true><<<sg, 32 * cule::kSWarps, e->ssmem, static_cast<cudaStream_t>(stream)>>>(p);
   } else {
     cule::debug_kernel<<<e->grid, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);

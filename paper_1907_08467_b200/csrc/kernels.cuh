@@ -63,6 +63,10 @@ struct Params {
   uint32_t slot_start[4];   // first slot of ROM r
   uint32_t first_env[4];    // first local env of ROM r (envs of ROM r are first_env[r] + n_roms*k)
   uint32_t idle_skip;       // exact idle-loop skip (cule_config.idle_skip; off by default)
+  // scalar engine
+  const uint64_t* srec;     // pre-decoded cartridge records, one per ROM image byte (scalar_predecode.h)
+  uint32_t use_rec;         // records staged into shared memory (they fit)
+  unsigned int* tickets;    // [2] env-slot ticket counter and finished-warp counter (self-resetting)
 };
 
 // The env a thread emulates.  Envs are laid out so that the lanes of a warp run the same ROM

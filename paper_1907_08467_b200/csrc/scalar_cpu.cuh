@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include "scalar_decode.h"
+#include "scalar_predecode.h"
 
 namespace cule {
 
@@ -150,24 +151,237 @@ __device__ __noinline__ uint32_t s_fetch_slow(SMach* M, uint32_t rom0, uint32_t 
 }
 
 // Run lane 0's machine until an event; `budget` (debug) counts instructions.
+//
+// Each instruction first looks up its pre-decoded record (scalar_predecode.h) at the PC; the
+// classes it covers run a short specialised case, everything else (and every PC outside the
+// cartridge window, or rec0 == 0) falls through to the general interpreter below, which is the
+// full machine model.  Phase A of an instruction samples at the end of the previous one: that is
+// fc, except right after a WSYNC stall, which is recorded as (ws_fc, ws_now) — fc strictly
+// increases within a call, so fc == ws_fc identifies the instruction right after the stall.
 template <bool kDebug>
 __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_t dtab0, uint32_t ram0, uint32_t lg0,
-                                            uint32_t log_lim, uint32_t cap_cycles, int32_t& budget) {
+                                            uint32_t log_lim, uint32_t cap_cycles, int32_t& budget,
+                                            uint32_t rec_all0) {
   uint32_t PC = M->PC, A = M->A, X = M->X, Y = M->Y, SP = M->SP;
   uint32_t C = M->C, V = M->V, D = M->D, I = M->I, nreg = M->nreg, zreg = M->zreg;
   uint32_t fc = M->fc, bank = M->bank, log_len = M->log_len;
-  uint32_t pend = M->t_phaseA / 3u;  // end cycle of the previous instruction (phase A at 3 pend)
+  uint32_t ws_fc = fc, ws_now = M->t_phaseA / 3u;  // phase A of the first instruction
   const uint32_t rom0 = rom_all0 + M->rom0;
+  // records staged (rec_all0 != 0): else every instruction takes the general path and the record
+  // load reads a fixed in-bounds word (the decode table)
+  const uint32_t recmask = rec_all0 != 0u ? 0x1000u : 0u;
+  const uint32_t offmask = rec_all0 != 0u ? 0xFFFFFFFFu : 0u;
+  const uint32_t rec0 = rec_all0 != 0u ? rec_all0 + 8u * M->rom0 : dtab0;
   const uint32_t is_f8 = M->is_f8;
   const uint32_t flim = is_f8 ? 0xFF5u : 0xFFDu;  // fast fetch: pc..pc+2 inside the page, no hotspot
   const uint32_t hlim = is_f8 ? 0xFF7u : 0xFFFu;  // fast data read: no hotspot
   uint32_t ev = SE_NONE;
-  // idle-loop skip (exact): the previous instruction, if it was a plain timer read
-  uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u;
+  // idle-loop skip (exact): the last plain timer read (PC, cycles, cycles its value holds, end)
+  uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
   const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
+  auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
+  auto adc = [&](uint32_t m) {
+    if (!D) {
+      const uint32_t t = A + m + C;
+      V = ((~(A ^ m) & (A ^ t)) >> 7) & 1u;
+      C = t >> 8;
+      A = t & 0xFFu;
+      nz(A);
+    } else {  // NMOS decimal (R#2)
+      uint32_t lo = (A & 0xFu) + (m & 0xFu) + C;
+      if (lo >= 0xAu) lo = ((lo + 6u) & 0xFu) + 0x10u;
+      uint32_t s = (A & 0xF0u) + (m & 0xF0u) + lo;
+      const int32_t sv = (int32_t)(int8_t)(A & 0xF0u) + (int32_t)(int8_t)(m & 0xF0u) + (int32_t)lo;
+      zreg = (A + m + C) & 0xFFu;
+      nreg = s;
+      V = (sv < -128 || sv > 127) ? 1u : 0u;
+      if (s >= 0xA0u) s += 0x60u;
+      C = s >= 0x100u ? 1u : 0u;
+      A = s & 0xFFu;
+    }
+  };
+  auto sbc = [&](uint32_t m) {
+    const uint32_t t = A + (m ^ 0xFFu) + C;
+    const uint32_t r = t & 0xFFu;
+    V = ((~(A ^ (m ^ 0xFFu)) & (A ^ t)) >> 7) & 1u;
+    if (D) {  // NMOS decimal: binary flags, BCD result (R#2)
+      int32_t lo = (int32_t)(A & 0xFu) - (int32_t)(m & 0xFu) + (int32_t)C - 1;
+      if (lo < 0) lo = ((lo - 6) & 0xF) - 0x10;
+      int32_t s = (int32_t)(A & 0xF0u) - (int32_t)(m & 0xF0u) + lo;
+      if (s < 0) s -= 0x60;
+      A = (uint32_t)s & 0xFFu;
+    } else {
+      A = r;
+    }
+    C = t >> 8;
+    nz(r);
+  };
+  auto cmp = [&](uint32_t r, uint32_t m) { C = r >= m ? 1u : 0u; nz((r - m) & 0xFFu); };
+  auto getP = [&]() {
+    return (nreg & 0x80u) | (V << 6) | 0x30u | (D << 3) | (I << 2) | ((zreg & 0xFFu) == 0u ? 2u : 0u) | C;
+  };
+  // branch condition of K_BR / C_BR: flag (0 N 1 V 2 C 3 Z) == taken-when bit
+  auto br_taken = [&](uint32_t aux) {
+    const uint32_t f = aux & 3u;
+    const uint32_t fl = f == 0u ? (nreg >> 7) & 1u : (f == 1u ? V : (f == 2u ? C : ((zreg & 0xFFu) == 0u ? 1u : 0u)));
+    return fl == ((aux >> 2) & 1u);
+  };
   for (;;) {
     if (kDebug && budget <= 0) { ev = SE_BUDGET; break; }
-    const uint32_t pc0 = PC, bank0 = bank;
+    const uint32_t pc0 = PC;
+    {
+      // ---- fast path: pre-decoded record -------------------------------------------------
+      uint32_t lo, hi;
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec0 + ((((bank << 12) | (pc0 & 0xFFFu)) << 3) & offmask)));
+      const uint32_t cls = (pc0 & recmask) ? (lo >> pd::CLS) & 31u : (uint32_t)C_GEN;
+      uint32_t now = fc + ((lo >> pd::CYC) & 0xFu);
+      uint32_t nPC = pc0 + ((lo >> pd::LEN) & 3u);
+      const uint32_t aux = (lo >> pd::AUX) & 7u;
+      const uint32_t opnd = hi & 0xFFFFu;
+      // data operand: RAM[(opnd + ix) & 0x7F] (zero page: bit 7 of opnd + ix selects RAM, else
+      // the general path) or the cartridge byte (opnd + ix) & 0xFFF of the bank (page-cross +1)
+      uint32_t t = opnd + __byte_perm(X | (Y << 8), 0u, hi >> 16);
+      uint32_t v = 0u;
+      auto rd_operand = [&]() -> bool {
+        if (lo & pd::RAM) {
+          if (!(t & 0x80u)) return false;
+          v = ld_ram(ram0 + (t & 0x7Fu));
+        } else {
+          v = ld_ro8(rec0 + (((bank << 12) | (t & 0xFFFu)) << 3));
+          now += (lo & pd::PEN) ? ((t ^ opnd) >> 8) & 1u : 0u;
+        }
+        return true;
+      };
+      auto ram_addr = [&]() -> bool { return (t & 0x80u) != 0u; };
+      switch (cls) {
+        case C_ORA: if (!rd_operand()) goto general; A |= v; nz(A); break;
+        case C_AND: if (!rd_operand()) goto general; A &= v; nz(A); break;
+        case C_EOR: if (!rd_operand()) goto general; A ^= v; nz(A); break;
+        case C_ADC: if (!rd_operand()) goto general; adc(v); break;
+        case C_SBC: if (!rd_operand()) goto general; sbc(v); break;
+        case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
+        case C_BIT: if (!rd_operand()) goto general; nreg = v; zreg = A & v; V = (v >> 6) & 1u; break;
+        case C_LD:
+          if (!rd_operand()) goto general;
+          A = (aux & 1u) ? v : A;
+          X = (aux & 2u) ? v : X;
+          Y = (aux & 4u) ? v : Y;
+          nz(v);
+          break;
+        case C_NOPR: if (!rd_operand()) goto general; break;
+        case C_TLD: {  // RIOT timer, closed form (R#24); the read is an idle-loop head candidate
+          const int32_t et = (int32_t)now - M->tW;
+          const uint32_t tV = M->tV, tS = M->tS;
+          const int32_t VI = (int32_t)(tV << tS);
+          uint32_t ff = 0u;
+          if (opnd & 1u) {
+            v = et > VI ? 0x80u : 0u;
+            ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
+          } else if (et <= VI) {
+            const int32_t q = (et + (1 << tS) - 1) >> tS;
+            v = (tV - (uint32_t)q) & 0xFFu;
+            ff = (uint32_t)((q << tS) - et);
+          } else {
+            v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
+          }
+          A = (aux & 1u) ? v : A;
+          X = (aux & 2u) ? v : X;
+          Y = (aux & 4u) ? v : Y;
+          nz(v);
+          pff = ff & skip_mask;
+          ppc = pc0;
+          pn = now - fc;
+          pfe = now;
+        } break;
+        case C_STRAM:
+          if (!ram_addr()) goto general;
+          st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
+          break;
+        case C_STTIA: {
+          const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
+          st_log(lg0 + 4u * log_len, ((3u * now) << 14) | ((lo >> pd::REG) << 8) | wv);
+          ++log_len;
+          if (log_len > log_lim) {
+            PC = nPC & 0xFFFFu;
+            fc = now;
+            if (kDebug) --budget;
+            if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; }
+            else ev = SE_LOGFULL;
+            goto out;
+          }
+        } break;
+        case C_WSYNC:  // stall to the next line start (R#5)
+          ws_now = now;
+          now = ((now + 75u) / 76u) * 76u;
+          ws_fc = now;
+          break;
+        case C_INC: case C_DEC: case C_ASL: case C_LSR: case C_ROL: case C_ROR: {
+          if (!ram_addr()) goto general;
+          const uint32_t a = ram0 + (t & 0x7Fu);
+          const uint32_t m = ld_ram(a);
+          uint32_t r;
+          if (cls == C_INC) r = (m + 1u) & 0xFFu;
+          else if (cls == C_DEC) r = (m - 1u) & 0xFFu;
+          else if (cls == C_ASL) { C = m >> 7; r = (m << 1) & 0xFFu; }
+          else if (cls == C_LSR) { C = m & 1u; r = m >> 1; }
+          else if (cls == C_ROL) { r = ((m << 1) | C) & 0xFFu; C = m >> 7; }
+          else { r = (m >> 1) | (C << 7); C = m & 1u; }
+          nz(r);
+          st_ram(a, r);
+        } break;
+        case C_INR: {
+          const uint32_t r = (((aux & 1u) ? Y : X) + ((aux & 2u) ? 0xFFu : 1u)) & 0xFFu;
+          X = (aux & 1u) ? X : r;
+          Y = (aux & 1u) ? r : Y;
+          nz(r);
+        } break;
+        case C_TR: {
+          const uint32_t s = aux & 3u, d = lo >> pd::REG;
+          const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
+          A = d == 0u ? r : A;
+          X = d == 1u ? r : X;
+          Y = d == 2u ? r : Y;
+          SP = d == 3u ? r : SP;
+          if (aux & 4u) nz(r);
+        } break;
+        case C_FLAG: {
+          const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
+          C = f == 0u ? b : C;
+          I = f == 1u ? b : I;
+          D = f == 2u ? b : D;
+          V = f == 3u ? b : V;
+        } break;
+        case C_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; nz(A); break;
+        case C_LSRA: C = A & 1u; A >>= 1; nz(A); break;
+        case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
+        case C_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
+        case C_NOP: break;
+        case C_BR:
+          if (br_taken(aux)) {
+            const uint32_t from = nPC & 0xFFFFu;
+            const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)opnd) & 0xFFFFu;
+            now += 1u + (((tgt ^ from) >> 8) & 1u);
+            nPC = tgt;
+            // idle-loop skip: [timer read; branch back to it] (see the general path)
+            if (!kDebug && pff != 0u && pfe == fc && tgt == ppc && now < cap_cycles) {
+              const uint32_t P = pn + (now - fc);
+              const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
+              now += j * P;
+            }
+          }
+          break;
+        case C_JMP: nPC = opnd; break;
+        default: goto general;
+      }
+      PC = nPC & 0xFFFFu;
+      fc = now;
+      if (kDebug) --budget;
+      if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; break; }  // runaway: fc / 76 >= line_cap
+      continue;
+    }
+  general : {
+    const uint32_t bank0 = bank;
+    const uint32_t pend = fc == ws_fc ? ws_now : fc;  // end cycle of the previous instruction
     uint32_t now = fc;
     uint32_t bad = 0u;  // bit 8 set: a collision read must wait for the TIA (abort)
     // full bus read (phase A: T = 3 pend; phase C: T = 3 now)
@@ -265,47 +479,6 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           s_wr_slow(M, a, val, now);  // RIOT
         }
       };
-      auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
-      auto adc = [&](uint32_t m) {
-        if (!D) {
-          const uint32_t t = A + m + C;
-          V = ((~(A ^ m) & (A ^ t)) >> 7) & 1u;
-          C = t >> 8;
-          A = t & 0xFFu;
-          nz(A);
-        } else {  // NMOS decimal (R#2)
-          uint32_t lo = (A & 0xFu) + (m & 0xFu) + C;
-          if (lo >= 0xAu) lo = ((lo + 6u) & 0xFu) + 0x10u;
-          uint32_t s = (A & 0xF0u) + (m & 0xF0u) + lo;
-          const int32_t sv = (int32_t)(int8_t)(A & 0xF0u) + (int32_t)(int8_t)(m & 0xF0u) + (int32_t)lo;
-          zreg = (A + m + C) & 0xFFu;
-          nreg = s;
-          V = (sv < -128 || sv > 127) ? 1u : 0u;
-          if (s >= 0xA0u) s += 0x60u;
-          C = s >= 0x100u ? 1u : 0u;
-          A = s & 0xFFu;
-        }
-      };
-      auto sbc = [&](uint32_t m) {
-        const uint32_t t = A + (m ^ 0xFFu) + C;
-        const uint32_t r = t & 0xFFu;
-        V = ((~(A ^ (m ^ 0xFFu)) & (A ^ t)) >> 7) & 1u;
-        if (D) {  // NMOS decimal: binary flags, BCD result (R#2)
-          int32_t lo = (int32_t)(A & 0xFu) - (int32_t)(m & 0xFu) + (int32_t)C - 1;
-          if (lo < 0) lo = ((lo - 6) & 0xF) - 0x10;
-          int32_t s = (int32_t)(A & 0xF0u) - (int32_t)(m & 0xF0u) + lo;
-          if (s < 0) s -= 0x60;
-          A = (uint32_t)s & 0xFFu;
-        } else {
-          A = r;
-        }
-        C = t >> 8;
-        nz(r);
-      };
-      auto cmp = [&](uint32_t r, uint32_t m) { C = r >= m ? 1u : 0u; nz((r - m) & 0xFFu); };
-      auto getP = [&]() {
-        return (nreg & 0x80u) | (V << 6) | 0x30u | (D << 3) | (I << 2) | ((zreg & 0xFFu) == 0u ? 2u : 0u) | C;
-      };
       // ---- operation ---------------------------------------------------------------------
       switch (kind) {
         case K_NOP: break;
@@ -362,16 +535,16 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           V = f == 3u ? b : V;
         } break;
         case K_BR: {
-          const uint32_t flags4 = ((nreg >> 7) & 1u) | (V << 1) | (C << 2) | ((zreg & 0xFFu) == 0u ? 8u : 0u);
-          if (((flags4 >> (aux & 3u)) & 1u) == ((aux >> 2) & 1u)) {
+          if (br_taken(aux)) {
             const uint32_t from = nPC & 0xFFFFu;
             const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
             now += 1u + (((tgt ^ from) >> 8) & 1u);
             nPC = tgt;
             // idle-loop skip: [timer read; branch back to it] — later iterations whose read
             // falls in the same constant interval repeat this one exactly, so only time
-            // advances (stopping short of the runaway cap, which the loop then reaches normally)
-            if (!kDebug && pff != 0u && tgt == ppc && (pc0 & 0x1000u) && now < cap_cycles) {
+            // advances (stopping short of the runaway cap, which the loop then reaches normally).
+            // pfe == fc: the read was the instruction right before this branch.
+            if (!kDebug && pff != 0u && pfe == fc && tgt == ppc && (pc0 & 0x1000u) && now < cap_cycles) {
               const uint32_t P = pn + (now - fc);
               const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
               now += j * P;
@@ -449,13 +622,11 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       if (d & sk::WR) wr(ea, wv);
       if (kDebug) --budget;
       // idle-loop head candidate: plain timer read in cartridge code
-      pff = (d & sk::PLAIN) ? (ff & skip_mask) : 0u;
-      ppc = pc0;
-      pn = n;
+      if (d & sk::PLAIN) { pff = ff & skip_mask; ppc = pc0; pn = n; pfe = now; }
       // ---- end of instruction (R#4, R#5) --------------------------------------------------
       PC = nPC & 0xFFFFu;
-      pend = now;
-      fc = fw != 0xFFFFFFFFu ? fw : now;
+      if (fw != 0xFFFFFFFFu) { ws_now = now; ws_fc = fw; fc = fw; }
+      else fc = now;
       if (fc >= cap_cycles || xf != 0u || log_len > log_lim) {
         if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; }  // runaway: fc / 76 >= line_cap
         else ev = xf ? SE_FRAME : SE_LOGFULL;
@@ -468,10 +639,11 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
     ev = SE_COLL;
     break;
   }
+  }
 out:
   M->PC = PC; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
   M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
-  M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * pend;
+  M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
   return ev;
 }
 

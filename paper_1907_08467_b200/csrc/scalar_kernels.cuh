@@ -11,9 +11,9 @@
 #include "scalar_cpu.cuh"
 #include "scalar_tia.cuh"
 
-// min resident blocks (4 warps each) per SM for the scalar kernel: 7 -> 28 warps, <= 72 registers
-#ifndef CULE_SMINB
-#define CULE_SMINB 7
+// warps per block of the scalar kernel: one block of 28 warps per SM (<= 72 registers per thread)
+#ifndef CULE_SWARPS
+#define CULE_SWARPS 28
 #endif
 
 namespace cule {
@@ -22,12 +22,14 @@ namespace cule {
 constexpr uint32_t kSLogCap = 128;
 constexpr uint32_t kSOffTia = 128, kSOffMach = 176, kSOffStg = 304, kSOffLog = 384;
 constexpr uint32_t kSWarpBytes = kSOffLog + 4 * kSLogCap;
-constexpr uint32_t kSWarps = 4;  // warps (envs) per block
+constexpr uint32_t kSWarps = CULE_SWARPS;  // warps per block (each warp emulates one env at a time)
 constexpr uint32_t kSmSDecode = kSmRom;  // scalar decode table [256] u64 right after the gray LUT
 constexpr uint32_t kSDecBytes = 2048;
 
-__host__ __device__ __forceinline__ size_t scalar_smem_bytes(uint32_t rom_bytes) {
-  return kSmSDecode + kSDecBytes + rom_bytes + (size_t)kSWarps * kSWarpBytes;
+// [header + gray][decode table][ROM images][records: 8 B per ROM byte, if staged][per-warp areas]
+__host__ __device__ __forceinline__ size_t scalar_rec_off(uint32_t rom_bytes) { return kSmSDecode + kSDecBytes + rom_bytes; }
+__host__ __device__ __forceinline__ size_t scalar_smem_bytes(uint32_t rom_bytes, bool use_rec) {
+  return scalar_rec_off(rom_bytes) + (use_rec ? (size_t)kRecBytes * rom_bytes : 0) + (size_t)kSWarps * kSWarpBytes;
 }
 
 __device__ __forceinline__ bool env_of_slot(const Params& p, uint32_t s, uint32_t& i) {
@@ -129,7 +131,8 @@ template <bool kGray, bool kDebug>
 __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, const uint64_t* dtab, uint8_t* ram,
                                               uint32_t* lg, uint32_t* tw, uint32_t cap_cycles, uint32_t lane,
                                               uint32_t nframes, uint8_t* frame_out, uint32_t& episode_frames,
-                                              int32_t budget, uint32_t ystart, const uint8_t* gray) {
+                                              int32_t budget, uint32_t ystart, const uint8_t* gray,
+                                              uint32_t rec_s) {
   const uint32_t fill = kGray ? (uint32_t)gray[0] * 0x01010101u : 0u;
   RowBuf rb;
   rb.fill = fill;
@@ -153,7 +156,7 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
                  lg_s = smem_addr(lg);
   for (;;) {
     uint32_t ev = SE_NONE;
-    if (lane == 0u) ev = run_cpu<kDebug>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget);
+    if (lane == 0u) ev = run_cpu<kDebug>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget, rec_s);
     ev = __shfl_sync(kFull, ev, 0);
     __syncwarp();
     const uint32_t n = M->log_len;
@@ -191,34 +194,33 @@ __device__ __forceinline__ void stage_block_s(const Params& p, uint8_t* smem) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, kSDecBytes + 128u + p.rom_bytes);
+    mbar_expect_tx(bar, kSDecBytes + 128u + p.rom_bytes * (p.use_rec ? 1u + kRecBytes : 1u));
     bulk_g2s(smem + kSmSDecode, p.sdecode, kSDecBytes, bar);
     bulk_g2s(smem + kSmGray, p.gray, 128u, bar);
+    uint8_t* rec = smem + scalar_rec_off(p.rom_bytes);
     for (uint32_t r = 0; r < p.n_roms; ++r) {
       const uint32_t len = ((p.f8_mask >> r) & 1u) ? 8192u : 4096u;
       bulk_g2s(smem + kSmSDecode + kSDecBytes + p.rom_off[r], p.roms + p.rom_off[r], len, bar);
+      if (p.use_rec) bulk_g2s(rec + kRecBytes * p.rom_off[r], p.srec + p.rom_off[r], kRecBytes * len, bar);
     }
   }
   __syncthreads();
   mbar_wait(bar, 0);
 }
 
+// one env for one step (or one debug budget), run by the whole warp
 template <bool kGray, bool kDebug>
-__global__ void __launch_bounds__(32 * kSWarps, CULE_SMINB) scalar_kernel(Params p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  stage_block_s(p, smem);
-  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+__device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t lane, const uint8_t* smem,
+                                           uint8_t* wb) {
   const uint8_t* rom_all = smem + kSmSDecode + kSDecBytes;
   const uint64_t* dtab = reinterpret_cast<const uint64_t*>(smem + kSmSDecode);
-  uint8_t* wb = smem + kSmSDecode + kSDecBytes + p.rom_bytes + wib * kSWarpBytes;
+  const uint32_t rec_s = p.use_rec ? smem_addr(smem + scalar_rec_off(p.rom_bytes)) : 0u;
   uint8_t* ram = wb;
   uint32_t* tw = reinterpret_cast<uint32_t*>(wb + kSOffTia);
   SMach* M = reinterpret_cast<SMach*>(wb + kSOffMach);
   uint8_t* stg = wb + kSOffStg;
   uint32_t* lg = reinterpret_cast<uint32_t*>(wb + kSOffLog);
   const uint8_t* gray = kGray ? smem + kSmGray : nullptr;
-  uint32_t i = 0;
-  if (!env_of_slot(p, blockIdx.x * kSWarps + wib, i)) return;  // whole warp
   const size_t N = p.N;
   uint4* st = reinterpret_cast<uint4*>(p.state);
   // state load: lane k < 13 fetches chunk k (header 0-3, RAM 4-11, bookkeeping 12)
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(32 * kSWarps, CULE_SMINB) scalar_kernel(Params
                               : (kGray ? p.staging + (size_t)i * (2 * kFrameBytes) : p.obs + (size_t)i * kFrameBytes);
   const int32_t status = simulate_s<kGray, kDebug>(M, rom_all, dtab, ram, lg, tw, 76u * p.line_cap, lane,
                                                    kDebug ? 1u : p.fs, frame_out, episode_frames, p.debug_instr,
-                                                   p.ystart, gray);
+                                                   p.ystart, gray, rec_s);
   if (kDebug) {
     if (lane == 0u) {
       if (status == RUN_JAM) M->fault = 1u;
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(32 * kSWarps, CULE_SMINB) scalar_kernel(Params
     __syncwarp();
     if (lane < 12u) st[lane * N + i] = lane < 4u ? reinterpret_cast<const uint4*>(stg)[lane]
                                                  : reinterpret_cast<const uint4*>(ram)[lane - 4u];
+    __syncwarp();
     return;
   }
   // a6: reward and done, once at step end (R#19); a7: reset from the cache
@@ -313,6 +316,34 @@ __global__ void __launch_bounds__(32 * kSWarps, CULE_SMINB) scalar_kernel(Params
     }
   } else if (fault) {
     warp_zero(p.obs + (size_t)i * kFrameBytes, kFrameBytes, lane);
+  }
+  __syncwarp();
+}
+
+// Persistent blocks: every warp takes env slots from a ticket counter until they run out, so
+// envs of different lengths balance across the SMs and the staged ROM/record images are reused.
+// The last warp to finish resets the counters for the next launch on the stream.
+template <bool kGray, bool kDebug>
+__global__ void __launch_bounds__(32 * kSWarps, 1) scalar_kernel(Params p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  stage_block_s(p, smem);
+  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  const size_t wb_off = scalar_smem_bytes(p.rom_bytes, p.use_rec != 0u) - (size_t)(kSWarps - wib) * kSWarpBytes;
+  uint8_t* wb = smem + wb_off;
+  for (;;) {
+    uint32_t s = 0;
+    if (lane == 0u) s = atomicAdd(&p.tickets[0], 1u);
+    s = __shfl_sync(kFull, s, 0);
+    uint32_t i = 0;
+    if (!env_of_slot(p, s, i)) break;
+    scalar_env<kGray, kDebug>(p, i, lane, smem, wb);
+  }
+  if (lane == 0u) {
+    const uint32_t total = gridDim.x * kSWarps;
+    if (atomicAdd(&p.tickets[1], 1u) == total - 1u) {
+      atomicExch(&p.tickets[0], 0u);
+      atomicExch(&p.tickets[1], 0u);
+    }
   }
 }
 

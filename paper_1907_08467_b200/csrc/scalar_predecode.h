@@ -1,0 +1,178 @@
+// scalar_predecode.h — host-side pre-decoding of the cartridge for the scalar engine's fast path.
+//
+// The ROM is constant (PAPER.md P:266-267 keeps it in constant memory for the same reason), so
+// every byte offset of every 4 KB bank can be decoded once, at cule_create, as if an instruction
+// started there.  One 8-byte record per ROM byte holds everything the interpreter needs to run
+// that instruction without touching the decode table: the operation class (one case of the
+// fast-path switch), length, base cycles, page-cross rule, register selector, the operand and
+// the index selector.  Byte 0 of the record is the ROM byte itself, so data reads from the
+// cartridge (tables, immediates) read the record array.
+//
+// The class also folds in what the address alone decides: a direct (zero-page or absolute)
+// operand is statically RAM, cartridge, TIA or RIOT, so the fast path never decodes the bus for
+// it.  Anything the fast path does not cover — pointer modes, stack and interrupt operations,
+// TIA reads (collision latches), bank-switch hotspots, fetches that cross the end of the 4 KB
+// window, JAM — is class GEN and runs through the general interpreter (scalar_cpu.cuh), which
+// implements the full machine model of DESIGN.md §2.  The records change no semantics: they are
+// a cache of the decode of constant bytes.
+#pragma once
+#include <stdint.h>
+
+#include "decode_table.h"
+#include "scalar_decode.h"
+
+namespace cule {
+
+namespace pd {
+// record word lo
+constexpr uint32_t CLS = 8;     // 5 bits: class
+constexpr uint32_t LEN = 13;    // 2 bits
+constexpr uint32_t CYC = 15;    // 4 bits: base cycles
+constexpr uint32_t PEN = 1u << 19;  // +1 cycle when the indexed address crosses a page
+constexpr uint32_t AUX = 20;    // 3 bits: register selector (see classes)
+constexpr uint32_t RAM = 1u << 23;  // the operand addresses RAM (else the cartridge)
+constexpr uint32_t REG = 24;    // 8 bits: TIA register (C_STTIA)
+// record word hi: bits 0-15 operand, bits 16-31 index byte-permute selector (sk::SEL_*)
+}  // namespace pd
+
+// fast-path classes; 0 = general interpreter
+enum PClass : uint32_t {
+  C_GEN = 0,
+  // reads: v = RAM[(opnd + ix) & 0x7F] (RAM; needs bit 7 of opnd + ix, else GEN) or the
+  // cartridge byte at offset (opnd + ix) & 0xFFF of the current bank (immediates: opnd = the
+  // offset of the operand byte); AUX = register (C_CMP: 0 A 1 X 2 Y, C_LD: bit mask 1 A 2 X 4 Y)
+  C_ORA, C_AND, C_EOR, C_ADC, C_SBC, C_CMP, C_BIT, C_LD, C_NOPR,
+  C_TLD,    // LDA/LDX/LDY/LAX of INTIM/TIMINT (absolute, RIOT timer closed form)
+  C_STRAM,  // store to RAM (zero page, zp indexed, or absolute RAM); AUX 0 A 1 X 2 Y 3 A&X
+  C_STTIA,  // store to a TIA register with a picture effect (direct): log append
+  C_WSYNC,  // store to WSYNC (direct)
+  C_INC, C_DEC, C_ASL, C_LSR, C_ROL, C_ROR,  // read-modify-write of RAM
+  C_INR,    // INX/INY/DEX/DEY, AUX as K_INR
+  C_TR,     // transfers, AUX bits 0-1 source, bit 2 (set N,Z) — destination in REG field
+  C_FLAG,   // flag set/clear, AUX as K_FLAG
+  C_ASLA, C_LSRA, C_ROLA, C_RORA,
+  C_NOP,    // implied NOP
+  C_BR,     // conditional branch, AUX as K_BR
+  C_JMP,    // JMP absolute
+  C_COUNT
+};
+static_assert(C_COUNT <= 32, "class field is 5 bits");
+
+constexpr uint32_t kRecBytes = 8;
+
+// decode the record for an instruction starting at bank offset o of a 4 KB bank image
+inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const uint64_t* stab) {
+  const uint32_t op = bank[o];
+  const uint64_t ent = stab[op];
+  const uint32_t d = (uint32_t)ent, e = (uint32_t)(ent >> 32);
+  const uint32_t kind = e & 0xFFu, aux = (e >> sk::AUX) & 0x7Fu;
+  const uint32_t len = (d >> sk::LEN) & 3u, cyc = (d >> sk::CYC) & 0xFu;
+  const uint32_t sel = d & 0xFFFFu;
+  const uint32_t b1 = o + 1 <= 0xFFFu ? bank[o + 1] : 0u, b2 = o + 2 <= 0xFFFu ? bank[o + 2] : 0u;
+  const uint32_t base = b1 | (b2 << 8);
+  uint32_t cls = C_GEN, opnd = 0, raux = 0, reg = 0;
+  bool ram = false, pen = (d & sk::PEN) != 0u;
+  // the whole instruction must be fetched from this bank window without touching a hotspot
+  bool fast = kind != K_JAM && o + len - 1 <= 0xFFFu;
+  if (f8)
+    for (uint32_t k = 0; k < len; ++k)
+      if (o + k == 0xFF8u || o + k == 0xFF9u) fast = false;
+  const bool zp = (d & sk::ZP) != 0u, ptr = (d & (sk::PTRZ | sk::PTRA)) != 0u;
+  const bool imm = len == 2 && !zp && !ptr && kind != K_BR && !(d & sk::RD) && !(d & sk::WR);
+  const bool indexed = sel != sk::SEL_NONE;
+  // classify the operand of a data access: 0 none/GEN, 1 RAM, 2 cartridge, 3 TIA (direct),
+  // 4 RIOT timer (direct)
+  auto where = [&]() -> int {
+    if (ptr) return 0;
+    if (zp) {
+      if (indexed) return 1;  // zp,X / zp,Y: RAM decided at run time (bit 7 of b1 + index)
+      return (b1 & 0x80u) ? 1 : 3;
+    }
+    const uint32_t a = base & 0x1FFFu;
+    if (!indexed) {
+      if ((a & 0x1280u) == 0x0080u) return 1;
+      if (a & 0x1000u) return (f8 && (a & 0x1FFEu) == 0x1FF8u) ? 0 : 2;
+      if (!(a & 0x1080u)) return 3;
+      if ((a & 0x1284u) == 0x0284u) return 4;
+      return 0;
+    }
+    // abs,X / abs,Y: every index 0..255 must stay in the window of this bank, clear of hotspots
+    if (!(a & 0x1000u)) return 0;
+    const uint32_t lo = a & 0xFFFu;
+    if (lo + 255u > 0xFFFu) return 0;
+    if (f8 && lo + 255u >= 0xFF8u) return 0;
+    return 2;
+  };
+  if (fast) {
+    switch (kind) {
+      case K_ORA: case K_AND: case K_EOR: case K_ADC: case K_SBC: case K_CMP: case K_BIT: case K_LD:
+      case K_NOP: {
+        if (kind == K_NOP && len == 1) { cls = C_NOP; break; }
+        const uint32_t rcls = kind == K_ORA ? C_ORA : kind == K_AND ? C_AND : kind == K_EOR ? C_EOR :
+                              kind == K_ADC ? C_ADC : kind == K_SBC ? C_SBC : kind == K_CMP ? C_CMP :
+                              kind == K_BIT ? C_BIT : kind == K_LD ? C_LD : C_NOPR;
+        raux = aux & 7u;
+        if (imm) { cls = rcls; opnd = o + 1; break; }
+        const int w = where();
+        if (w == 1) { cls = rcls; ram = true; opnd = zp ? b1 : (base & 0x7Fu) | 0x80u; }
+        else if (w == 2) { cls = rcls; opnd = base & 0xFFFu; }
+        else if (w == 4 && kind == K_LD && !indexed) { cls = C_TLD; opnd = base & 0x1FFFu; }
+        break;
+      }
+      case K_ST: {
+        const int w = where();
+        raux = aux & 3u;
+        if (w == 1) { cls = C_STRAM; ram = true; opnd = zp ? b1 : (base & 0x7Fu) | 0x80u; }
+        else if (w == 3 && !indexed) {
+          const uint32_t r = (zp ? b1 : base) & 0x3Fu;
+          // TIA writes with a picture effect: 0x01, 0x04-0x14, 0x1B-0x2C (scalar_cpu.cuh kTiaEffect)
+          const bool eff = r == 0x01u || (r >= 0x04u && r <= 0x14u) || (r >= 0x1Bu && r <= 0x2Cu);
+          if (eff) { cls = C_STTIA; reg = r; }
+          else if (r == 0x02u) cls = C_WSYNC;
+        }
+        break;
+      }
+      case K_INC: case K_DEC: case K_ASL: case K_LSR: case K_ROL: case K_ROR: {
+        if (where() == 1) {
+          cls = kind == K_INC ? C_INC : kind == K_DEC ? C_DEC : kind == K_ASL ? C_ASL :
+                kind == K_LSR ? C_LSR : kind == K_ROL ? C_ROL : C_ROR;
+          ram = true;
+          opnd = zp ? b1 : (base & 0x7Fu) | 0x80u;
+        }
+        break;
+      }
+      case K_INR: cls = C_INR; raux = aux & 3u; break;
+      case K_TR: cls = C_TR; raux = (aux & 3u) | ((aux & 16u) ? 4u : 0u); reg = (aux >> 2) & 3u; break;
+      case K_FLAG: cls = C_FLAG; raux = aux & 7u; break;
+      case K_ASLA: cls = C_ASLA; break;
+      case K_LSRA: cls = C_LSRA; break;
+      case K_ROLA: cls = C_ROLA; break;
+      case K_RORA: cls = C_RORA; break;
+      case K_BR: cls = C_BR; raux = aux & 7u; opnd = b1; break;
+      case K_JMP: if (!ptr) { cls = C_JMP; opnd = base; } break;
+      default: break;
+    }
+  }
+  uint32_t lo = op | (cls << pd::CLS) | (len << pd::LEN) | (cyc << pd::CYC) | (raux << pd::AUX) | (reg << pd::REG);
+  if (pen) lo |= pd::PEN;
+  if (ram) lo |= pd::RAM;
+  const uint32_t hi = (opnd & 0xFFFFu) | (sel << 16);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+// records for a packed ROM image: rec[i] describes an instruction starting at image byte i
+// (bank = i / 4096 within its ROM)
+inline void predecode_roms(const uint8_t* img, const uint32_t* rom_off, const uint32_t* rom_len, int n_roms,
+                           uint64_t* rec) {
+  uint64_t stab[256];
+  build_scalar_table(stab);
+  for (int r = 0; r < n_roms; ++r) {
+    const bool f8 = rom_len[r] == 8192u;
+    for (uint32_t b = 0; b < rom_len[r] / 4096u; ++b) {
+      const uint8_t* bank = img + rom_off[r] + 4096u * b;
+      for (uint32_t o = 0; o < 4096u; ++o) rec[rom_off[r] + 4096u * b + o] = predecode_one(bank, o, f8, stab);
+    }
+  }
+}
+
+}  // namespace cule
