@@ -278,14 +278,15 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   e->epw = choose_epw(num_envs);
   e->engine = choose_engine(num_envs);
   {
-    // records cost 8 B per ROM byte of shared memory: staged whenever they fit (all 4 KB and
-    // F8 combinations up to 4 x 4 KB / 2 x F8 + 1 x 4 KB); CULE_NO_REC=1 disables them
+    // records cost 8 B per ROM byte of shared memory: they fit for every combination up to
+    // 4 x 4 KB or 2 x F8 + 1 x 4 KB (CULE_NO_REC=1 pretends they do not)
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (optin <= 0) optin = 232448;
     const char* nr = getenv("CULE_NO_REC");
     e->use_rec = (!(nr && atoi(nr) == 1) && cule::scalar_smem_bytes(e->rom_bytes, true) <= (size_t)optin) ? 1u : 0u;
+    if (!e->use_rec) e->engine = 0;  // the scalar engine runs from the records: batched engine otherwise
     e->ssmem = cule::scalar_smem_bytes(e->rom_bytes, e->use_rec != 0u);
     const uint32_t need = ((uint32_t)num_envs + cule::kSWarps - 1) / cule::kSWarps;
     const uint32_t sms = (uint32_t)sm_count();

@@ -167,11 +167,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   uint32_t fc = M->fc, bank = M->bank, log_len = M->log_len;
   uint32_t ws_fc = fc, ws_now = M->t_phaseA / 3u;  // phase A of the first instruction
   const uint32_t rom0 = rom_all0 + M->rom0;
-  // records staged (rec_all0 != 0): else every instruction takes the general path and the record
-  // load reads a fixed in-bounds word (the decode table)
-  const uint32_t recmask = rec_all0 != 0u ? 0x1000u : 0u;
-  const uint32_t offmask = rec_all0 != 0u ? 0xFFFFFFFFu : 0u;
-  const uint32_t rec0 = rec_all0 != 0u ? rec_all0 + 8u * M->rom0 : dtab0;
+  const uint32_t rec0 = rec_all0 + 8u * M->rom0;  // pre-decoded records of this env's ROM
   const uint32_t is_f8 = M->is_f8;
   const uint32_t flim = is_f8 ? 0xFF5u : 0xFFDu;  // fast fetch: pc..pc+2 inside the page, no hotspot
   const uint32_t hlim = is_f8 ? 0xFF7u : 0xFFFu;  // fast data read: no hotspot
@@ -232,15 +228,37 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
     {
       // ---- fast path: pre-decoded record -------------------------------------------------
       uint32_t lo, hi;
-      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec0 + ((((bank << 12) | (pc0 & 0xFFFu)) << 3) & offmask)));
-      const uint32_t cls = (pc0 & recmask) ? (lo >> pd::CLS) & 31u : (uint32_t)C_GEN;
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec0 + (((bank << 12) | (pc0 & 0xFFFu)) << 3)));
+      const uint32_t cls = (pc0 & 0x1000u) ? (lo >> pd::CLS) & 31u : (uint32_t)C_GEN;
       uint32_t now = fc + ((lo >> pd::CYC) & 0xFu);
       uint32_t nPC = pc0 + ((lo >> pd::LEN) & 3u);
       const uint32_t aux = (lo >> pd::AUX) & 7u;
       const uint32_t opnd = hi & 0xFFFFu;
+      if (cls == C_BR) {  // the most frequent class, tested before the switch
+        const uint32_t src = (aux & 2u) ? ((aux & 1u) ? zreg : C) : ((aux & 1u) ? V : nreg);
+        if (((src & (lo >> pd::REG)) != 0u) == ((aux & 4u) != 0u)) {
+          const uint32_t from = nPC & 0xFFFFu;
+          const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)opnd) & 0xFFFFu;
+          now += 1u + (((tgt ^ from) >> 8) & 1u);
+          nPC = tgt;
+          // idle-loop skip: [timer read; branch back to it] (see the general path)
+          if (!kDebug && pff != 0u && pfe == fc && tgt == ppc && now < cap_cycles) {
+            const uint32_t P = pn + (now - fc);
+            const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
+            now += j * P;
+          }
+          // a runaway frame can only spin through a taken branch, a jump or the general path:
+          // the step kernel checks the cap there (a faulted env's state is replaced by the
+          // reset cache, so only the step of the fault matters); the debug entry checks it
+          // after every instruction
+          if (!kDebug && now >= cap_cycles) { PC = nPC; fc = now; M->fault = 2u; ev = SE_FAULT; break; }
+        }
+        goto fast_done;
+      }
+      {
       // data operand: RAM[(opnd + ix) & 0x7F] (zero page: bit 7 of opnd + ix selects RAM, else
       // the general path) or the cartridge byte (opnd + ix) & 0xFFF of the bank (page-cross +1)
-      uint32_t t = opnd + __byte_perm(X | (Y << 8), 0u, hi >> 16);
+      const uint32_t t = opnd + __byte_perm(X | (Y << 8), 0u, hi >> 16);
       uint32_t v = 0u;
       auto rd_operand = [&]() -> bool {
         if (lo & pd::RAM) {
@@ -248,8 +266,8 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           v = ld_ram(ram0 + (t & 0x7Fu));
         } else {
           v = ld_ro8(rec0 + (((bank << 12) | (t & 0xFFFu)) << 3));
-          now += (lo & pd::PEN) ? ((t ^ opnd) >> 8) & 1u : 0u;
         }
+        now += (lo & pd::PEN) ? ((t ^ opnd) >> 8) & 1u : 0u;
         return true;
       };
       auto ram_addr = [&]() -> bool { return (t & 0x80u) != 0u; };
@@ -269,7 +287,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           nz(v);
           break;
         case C_NOPR: if (!rd_operand()) goto general; break;
-        case C_TLD: {  // RIOT timer, closed form (R#24); the read is an idle-loop head candidate
+        case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
           const int32_t et = (int32_t)now - M->tW;
           const uint32_t tV = M->tV, tS = M->tS;
           const int32_t VI = (int32_t)(tV << tS);
@@ -284,10 +302,14 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           } else {
             v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
           }
-          A = (aux & 1u) ? v : A;
-          X = (aux & 2u) ? v : X;
-          Y = (aux & 4u) ? v : Y;
-          nz(v);
+          if (cls == C_TLD) {
+            A = (aux & 1u) ? v : A;
+            X = (aux & 2u) ? v : X;
+            Y = (aux & 4u) ? v : Y;
+            nz(v);
+          } else {
+            nreg = v; zreg = A & v; V = (v >> 6) & 1u;
+          }
           pff = ff & skip_mask;
           ppc = pc0;
           pn = now - fc;
@@ -356,27 +378,20 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
         case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
         case C_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
         case C_NOP: break;
-        case C_BR:
-          if (br_taken(aux)) {
-            const uint32_t from = nPC & 0xFFFFu;
-            const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)opnd) & 0xFFFFu;
-            now += 1u + (((tgt ^ from) >> 8) & 1u);
-            nPC = tgt;
-            // idle-loop skip: [timer read; branch back to it] (see the general path)
-            if (!kDebug && pff != 0u && pfe == fc && tgt == ppc && now < cap_cycles) {
-              const uint32_t P = pn + (now - fc);
-              const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
-              now += j * P;
-            }
-          }
+        case C_JMP:
+          nPC = opnd;
+          if (!kDebug && now >= cap_cycles) { PC = nPC; fc = now; M->fault = 2u; ev = SE_FAULT; goto out; }
           break;
-        case C_JMP: nPC = opnd; break;
         default: goto general;
       }
+      }
+    fast_done:
       PC = nPC & 0xFFFFu;
       fc = now;
-      if (kDebug) --budget;
-      if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; break; }  // runaway: fc / 76 >= line_cap
+      if (kDebug) {
+        --budget;
+        if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; break; }  // runaway: fc / 76 >= line_cap
+      }
       continue;
     }
   general : {

@@ -214,7 +214,7 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
                                            uint8_t* wb) {
   const uint8_t* rom_all = smem + kSmSDecode + kSDecBytes;
   const uint64_t* dtab = reinterpret_cast<const uint64_t*>(smem + kSmSDecode);
-  const uint32_t rec_s = p.use_rec ? smem_addr(smem + scalar_rec_off(p.rom_bytes)) : 0u;
+  const uint32_t rec_s = smem_addr(smem + scalar_rec_off(p.rom_bytes));  // records (always staged)
   uint8_t* ram = wb;
   uint32_t* tw = reinterpret_cast<uint32_t*>(wb + kSOffTia);
   SMach* M = reinterpret_cast<SMach*>(wb + kSOffMach);

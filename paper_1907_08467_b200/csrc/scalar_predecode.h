@@ -43,6 +43,7 @@ enum PClass : uint32_t {
   // offset of the operand byte); AUX = register (C_CMP: 0 A 1 X 2 Y, C_LD: bit mask 1 A 2 X 4 Y)
   C_ORA, C_AND, C_EOR, C_ADC, C_SBC, C_CMP, C_BIT, C_LD, C_NOPR,
   C_TLD,    // LDA/LDX/LDY/LAX of INTIM/TIMINT (absolute, RIOT timer closed form)
+  C_TBIT,   // BIT of INTIM/TIMINT (absolute)
   C_STRAM,  // store to RAM (zero page, zp indexed, or absolute RAM); AUX 0 A 1 X 2 Y 3 A&X
   C_STTIA,  // store to a TIA register with a picture effect (direct): log append
   C_WSYNC,  // store to WSYNC (direct)
@@ -52,7 +53,8 @@ enum PClass : uint32_t {
   C_FLAG,   // flag set/clear, AUX as K_FLAG
   C_ASLA, C_LSRA, C_ROLA, C_RORA,
   C_NOP,    // implied NOP
-  C_BR,     // conditional branch, AUX as K_BR
+  C_BR,     // conditional branch: AUX bits 0-1 source (0 nreg, 1 V, 2 C, 3 zreg), REG mask, AUX
+            // bit 2 = taken when (source & mask) != 0
   C_JMP,    // JMP absolute
   C_COUNT
 };
@@ -96,6 +98,9 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
       if ((a & 0x1284u) == 0x0284u) return 4;
       return 0;
     }
+    // abs,X / abs,Y based in zero-page RAM ($80-$FF): RAM decided at run time like zp,X (the
+    // sum stays below $200, so bit 7 alone separates RAM from the TIA mirror at $100-$17F)
+    if (a >= 0x80u && a <= 0xFFu) return 1;
     // abs,X / abs,Y: every index 0..255 must stay in the window of this bank, clear of hotspots
     if (!(a & 0x1000u)) return 0;
     const uint32_t lo = a & 0xFFFu;
@@ -114,9 +119,10 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
         raux = aux & 7u;
         if (imm) { cls = rcls; opnd = o + 1; break; }
         const int w = where();
-        if (w == 1) { cls = rcls; ram = true; opnd = zp ? b1 : (base & 0x7Fu) | 0x80u; }
+        if (w == 1) { cls = rcls; ram = true; opnd = zp ? b1 : (base & 0x7Fu) | 0x80u; }  // = base if indexed
         else if (w == 2) { cls = rcls; opnd = base & 0xFFFu; }
-        else if (w == 4 && kind == K_LD && !indexed) { cls = C_TLD; opnd = base & 0x1FFFu; }
+        else if (w == 4 && kind == K_LD) { cls = C_TLD; opnd = base & 0x1FFFu; }
+        else if (w == 4 && kind == K_BIT) { cls = C_TBIT; opnd = base & 0x1FFFu; }
         break;
       }
       case K_ST: {
@@ -148,7 +154,13 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
       case K_LSRA: cls = C_LSRA; break;
       case K_ROLA: cls = C_ROLA; break;
       case K_RORA: cls = C_RORA; break;
-      case K_BR: cls = C_BR; raux = aux & 7u; opnd = b1; break;
+      case K_BR: {  // taken iff ((flag source & REG mask) != 0) == AUX bit 2 (see C_BR)
+        const uint32_t f = aux & 3u, want = (aux >> 2) & 1u;
+        cls = C_BR;
+        reg = f == 0u ? 0x80u : (f == 3u ? 0xFFu : 0x01u);  // N: bit 7 of nreg; Z: zreg & 0xFF
+        raux = f | ((want ^ (f == 3u ? 1u : 0u)) << 2);
+        opnd = b1;
+      } break;
       case K_JMP: if (!ptr) { cls = C_JMP; opnd = base; } break;
       default: break;
     }

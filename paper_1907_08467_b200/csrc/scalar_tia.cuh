@@ -232,6 +232,9 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   const uint32_t h0 = t0 - l0 * 228u, h1 = t_to - l1 * 228u;
   const uint32_t xa0 = h0 > 68u ? h0 - 68u : 0u;
   const uint32_t xb1 = h1 > 68u ? h1 - 68u : 0u;
+  // a span inside one line with no visible clock (e.g. writes right after WSYNC, in HBLANK)
+  // neither collides nor draws, and cannot complete a row (that needs xb1 = 160 > xa0)
+  if (l1 == l0 && xb1 <= xa0) return;
   const bool vblank = t.f(0) != 0u;
   const bool need_coll = !vblank && t.open_pairs() != 0u;
   const uint32_t w0 = ystart, w1 = ystart + (uint32_t)kFrameH;
