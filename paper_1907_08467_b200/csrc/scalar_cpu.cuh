@@ -150,31 +150,26 @@ __device__ __noinline__ uint32_t s_fetch_slow(SMach* M, uint32_t rom0, uint32_t 
   return out | ((bad & 0x100u) ? (1u << 24) : 0u) | (bank << 25);
 }
 
-// Run lane 0's machine until an event; `budget` (debug) counts instructions.
-//
-// Each instruction first looks up its pre-decoded record (scalar_predecode.h) at the PC; the
-// classes it covers run a short specialised case, everything else (and every PC outside the
-// cartridge window, or rec0 == 0) falls through to the general interpreter below, which is the
-// full machine model.  Phase A of an instruction samples at the end of the previous one: that is
-// fc, except right after a WSYNC stall, which is recorded as (ws_fc, ws_now) — fc strictly
-// increases within a call, so fc == ws_fc identifies the instruction right after the stall.
-template <bool kDebug>
-__device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_t dtab0, uint32_t ram0, uint32_t lg0,
-                                            uint32_t log_lim, uint32_t cap_cycles, int32_t& budget,
-                                            uint32_t rec_all0) {
+constexpr uint32_t kGenCommitted = 0x100u;
+
+// One instruction through the general interpreter (the full machine model), on the machine
+// record in shared memory: registers and clocks in M, M->t_phaseA = 3 x the cycle at which the
+// instruction's phase A samples.  Out of line, so the fast loop of run_cpu() keeps its
+// registers to itself.  Returns the event (SEvent), | kGenCommitted if the instruction completed
+// (a collision-latch read that must wait for the TIA commits nothing; JAM faults uncommitted).
+// The idle-loop skip is not applied here (skipping is optional and exact either way).
+__device__ __noinline__ uint32_t s_gen_one(SMach* M, uint32_t rom_all0, uint32_t dtab0, uint32_t ram0, uint32_t lg0,
+                                           uint32_t log_lim, uint32_t cap_cycles) {
   uint32_t PC = M->PC, A = M->A, X = M->X, Y = M->Y, SP = M->SP;
   uint32_t C = M->C, V = M->V, D = M->D, I = M->I, nreg = M->nreg, zreg = M->zreg;
   uint32_t fc = M->fc, bank = M->bank, log_len = M->log_len;
-  uint32_t ws_fc = fc, ws_now = M->t_phaseA / 3u;  // phase A of the first instruction
+  const uint32_t pend = M->t_phaseA / 3u;  // end cycle of the previous instruction
+  uint32_t pnext = pend;
   const uint32_t rom0 = rom_all0 + M->rom0;
-  const uint32_t rec0 = rec_all0 + 8u * M->rom0;  // pre-decoded records of this env's ROM
   const uint32_t is_f8 = M->is_f8;
   const uint32_t flim = is_f8 ? 0xFF5u : 0xFFDu;  // fast fetch: pc..pc+2 inside the page, no hotspot
   const uint32_t hlim = is_f8 ? 0xFF7u : 0xFFFu;  // fast data read: no hotspot
-  uint32_t ev = SE_NONE;
-  // idle-loop skip (exact): the last plain timer read (PC, cycles, cycles its value holds, end)
-  uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
-  const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
+  uint32_t ev = SE_NONE, committed = 0u;
   auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
   auto adc = [&](uint32_t m) {
     if (!D) {
@@ -222,6 +217,320 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
     const uint32_t fl = f == 0u ? (nreg >> 7) & 1u : (f == 1u ? V : (f == 2u ? C : ((zreg & 0xFFu) == 0u ? 1u : 0u)));
     return fl == ((aux >> 2) & 1u);
   };
+  const uint32_t pc0 = PC;
+  {
+    const uint32_t bank0 = bank;
+    uint32_t now = fc;
+    uint32_t bad = 0u;  // bit 8 set: a collision read must wait for the TIA (abort)
+    // full bus read (phase A: T = 3 pend; phase C: T = 3 now)
+    auto rd = [&](uint32_t addr, uint32_t T, uint32_t pa) -> uint32_t {
+      const uint32_t a = addr & 0x1FFFu;
+      if (a & 0x1000u) {
+        if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+        return ld_ro8(rom0 + (bank << 12) + (a & 0xFFFu));
+      }
+      if ((a & 0x0280u) == 0x0080u) return ld_ram(ram0 + (a & 0x7Fu));
+      const uint32_t r = s_rd_io(M, a, T, now, pa);
+      bad |= r;
+      return r & 0xFFu;
+    };
+    uint32_t op, b1, b2;
+    if ((pc0 & 0x1000u) && (pc0 & 0xFFFu) <= flim) {
+      const uint32_t p = rom0 + (bank << 12) + (pc0 & 0xFFFu);
+      op = ld_ro8(p); b1 = ld_ro8(p + 1u); b2 = ld_ro8(p + 2u);
+    } else {
+      const uint32_t f = s_fetch_slow(M, rom0, ram0, dtab0, pc0, bank, 3u * pend, now);
+      bank = f >> 25;
+      if (f & (1u << 24)) goto coll;
+      op = f & 0xFFu; b1 = (f >> 8) & 0xFFu; b2 = (f >> 16) & 0xFFu;
+    }
+    {
+      uint32_t d, e;  // decode entry (scalar_decode.h): d = mode/flags word, e = kind/aux word
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d), "=r"(e) : "r"(dtab0 + 8u * op));
+      const uint32_t kind = e & 0xFFu, aux = e >> sk::AUX;
+      uint32_t n = (d >> sk::CYC) & 0xFu;
+      uint32_t nPC = pc0 + ((d >> sk::LEN) & 3u);
+      // ---- phase A: effective address ------------------------------------------------------
+      const uint32_t ix = __byte_perm(X | (Y << 8), 0u, d);  // X, Y or 0
+      uint32_t base = b1 | (b2 << 8), ea;
+      if (!(d & (sk::PTRZ | sk::PTRA))) {
+        ea = (base + ix) & ((d & sk::ZP) ? 0xFFu : 0xFFFFu);
+      } else {  // (zp,X): index before the pointer; (zp),Y: after; JMP (abs): page-wrap bug
+        const bool pa = (d & sk::PTRA) != 0u, pre = (d & sk::ZP) != 0u;
+        const uint32_t z = (b1 + (pre ? ix : 0u)) & 0xFFu;
+        const uint32_t p0 = pa ? base : z;
+        const uint32_t p1 = pa ? ((base & 0xFF00u) | ((base + 1u) & 0xFFu)) : ((z + 1u) & 0xFFu);
+        const uint32_t lo = rd(p0, 3u * pend, 1u);
+        const uint32_t hi = rd(p1, 3u * pend, 1u);
+        if (bad & 0x100u) goto coll;
+        base = lo | (hi << 8);
+        ea = (base + (pre ? 0u : ix)) & 0xFFFFu;
+      }
+      n += ((d & sk::PEN) && ((ea ^ base) & 0x100u)) ? 1u : 0u;
+      now = fc + n;
+      // ---- phase C: data read ------------------------------------------------------------
+      uint32_t v = (d & sk::ACC) ? A : b1;
+      uint32_t ff = 0u;  // timer reads: cycles over which the value read stays the same
+      if (d & sk::RD) {
+        const uint32_t a = ea & 0x1FFFu;
+        const bool cart = (a & 0x1000u) != 0u;
+        if (cart ? (a & 0xFFFu) <= hlim : (a & 0x0280u) == 0x0080u) {
+          v = cart ? ld_ro8(rom0 + (bank << 12) + (a & 0xFFFu)) : ld_ram(ram0 + (a & 0x7Fu));
+        } else if ((a & 0x1284u) == 0x0284u) {  // RIOT timer, closed form (R#24)
+          const int32_t et = (int32_t)now - M->tW;
+          const uint32_t tV = M->tV, tS = M->tS;
+          const int32_t VI = (int32_t)(tV << tS);
+          if (a & 1u) {  // TIMINT: 0 up to the expiry, 0x80 after it
+            v = et > VI ? 0x80u : 0u;
+            ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
+          } else if (et <= VI) {  // INTIM while counting: constant up to the next interval edge
+            const int32_t q = (et + (1 << tS) - 1) >> tS;
+            v = (tV - (uint32_t)q) & 0xFFu;
+            ff = (uint32_t)((q << tS) - et);
+          } else {  // INTIM after the expiry: counts down every cycle
+            v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
+          }
+        } else {
+          v = rd(a, 3u * now, 0u);
+          if (bad & 0x100u) goto coll;
+        }
+      }
+      uint32_t wv = 0u, xf = 0u;  // xf: exit flags (2 VSYNC rose); fw: cycle after a WSYNC stall
+      uint32_t fw = 0xFFFFFFFFu;
+      auto wr = [&](uint32_t addr, uint32_t val) {
+        const uint32_t a = addr & 0x1FFFu;
+        if ((a & 0x1280u) == 0x0080u) {
+          st_ram(ram0 + (a & 0x7Fu), val & 0xFFu);
+        } else if (!(a & 0x1080u)) {  // TIA: effect registers go to the log (R#4)
+          const uint32_t r = a & 0x3Fu;
+          if ((kTiaEffect >> r) & 1ull) {
+            st_log(lg0 + 4u * log_len, ((3u * now) << 14) | (r << 8) | (val & 0xFFu));
+            ++log_len;
+          } else if (r == 0x02u) {
+            fw = ((now + 75u) / 76u) * 76u;  // WSYNC: stall to the next line start (R#5)
+          } else if (r == 0x00u) {
+            xf |= s_wr_slow(M, a, val, now);
+          }
+        } else if (a & 0x1000u) {
+          if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+        } else {
+          s_wr_slow(M, a, val, now);  // RIOT
+        }
+      };
+      // ---- operation ---------------------------------------------------------------------
+      switch (kind) {
+        case K_NOP: break;
+        case K_ORA: A |= v; nz(A); break;
+        case K_AND: A &= v; nz(A); break;
+        case K_EOR: A ^= v; nz(A); break;
+        case K_ADC: adc(v); break;
+        case K_SBC: sbc(v); break;
+        case K_CMP: cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
+        case K_BIT: nreg = v; zreg = A & v; V = (v >> 6) & 1u; break;
+        case K_LD:
+          A = (aux & 1u) ? v : A;
+          X = (aux & 2u) ? v : X;
+          Y = (aux & 4u) ? v : Y;
+          nz(v);
+          break;
+        case K_ST: wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))); break;
+        case K_ASL: C = v >> 7; wv = (v << 1) & 0xFFu; nz(wv); break;
+        case K_LSR: C = v & 1u; wv = v >> 1; nz(wv); break;
+        case K_ROL: wv = ((v << 1) | C) & 0xFFu; C = v >> 7; nz(wv); break;
+        case K_ROR: wv = (v >> 1) | (C << 7); C = v & 1u; nz(wv); break;
+        case K_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; nz(A); break;
+        case K_LSRA: C = A & 1u; A >>= 1; nz(A); break;
+        case K_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
+        case K_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
+        case K_INC: wv = (v + 1u) & 0xFFu; nz(wv); break;
+        case K_DEC: wv = (v - 1u) & 0xFFu; nz(wv); break;
+        case K_SLO: C = v >> 7; wv = (v << 1) & 0xFFu; A |= wv; nz(A); break;
+        case K_RLA: wv = ((v << 1) | C) & 0xFFu; C = v >> 7; A &= wv; nz(A); break;
+        case K_SRE: C = v & 1u; wv = v >> 1; A ^= wv; nz(A); break;
+        case K_RRA: wv = (v >> 1) | (C << 7); C = v & 1u; adc(wv); break;
+        case K_DCP: wv = (v - 1u) & 0xFFu; cmp(A, wv); break;
+        case K_ISB: wv = (v + 1u) & 0xFFu; sbc(wv); break;
+        case K_INR: {
+          const uint32_t r = (((aux & 1u) ? Y : X) + ((aux & 2u) ? 0xFFu : 1u)) & 0xFFu;
+          X = (aux & 1u) ? X : r;
+          Y = (aux & 1u) ? r : Y;
+          nz(r);
+        } break;
+        case K_TR: {
+          const uint32_t s = aux & 3u, t = (aux >> 2) & 3u;
+          const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
+          A = t == 0u ? r : A;
+          X = t == 1u ? r : X;
+          Y = t == 2u ? r : Y;
+          SP = t == 3u ? r : SP;
+          if (aux & 16u) nz(r);
+        } break;
+        case K_FLAG: {
+          const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
+          C = f == 0u ? b : C;
+          I = f == 1u ? b : I;
+          D = f == 2u ? b : D;
+          V = f == 3u ? b : V;
+        } break;
+        case K_BR: {
+          if (br_taken(aux)) {
+            const uint32_t from = nPC & 0xFFFFu;
+            const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
+            now += 1u + (((tgt ^ from) >> 8) & 1u);
+            nPC = tgt;
+          }
+        } break;
+        case K_JMP: nPC = ea; break;
+        case K_JSR: {
+          const uint32_t ret = (pc0 + 2u) & 0xFFFFu;
+          wr(0x100u | SP, ret >> 8); SP = (SP - 1u) & 0xFFu;
+          wr(0x100u | SP, ret & 0xFFu); SP = (SP - 1u) & 0xFFu;
+          nPC = ea;
+        } break;
+        case K_RTS: {
+          const uint32_t s1 = (SP + 1u) & 0xFFu, s2 = (SP + 2u) & 0xFFu;
+          const uint32_t lo = rd(0x100u | s1, 3u * now, 0u);
+          const uint32_t hi = rd(0x100u | s2, 3u * now, 0u);
+          if (bad & 0x100u) goto coll;
+          SP = s2;
+          nPC = (lo | (hi << 8)) + 1u;
+        } break;
+        case K_RTI: {
+          const uint32_t s1 = (SP + 1u) & 0xFFu, s2 = (SP + 2u) & 0xFFu, s3 = (SP + 3u) & 0xFFu;
+          const uint32_t p = rd(0x100u | s1, 3u * now, 0u);
+          const uint32_t lo = rd(0x100u | s2, 3u * now, 0u);
+          const uint32_t hi = rd(0x100u | s3, 3u * now, 0u);
+          if (bad & 0x100u) goto coll;
+          SP = s3;
+          nreg = p & 0x80u; V = (p >> 6) & 1u; D = (p >> 3) & 1u; I = (p >> 2) & 1u;
+          zreg = (p & 2u) ? 0u : 1u; C = p & 1u;
+          nPC = lo | (hi << 8);
+        } break;
+        case K_BRK: {
+          const uint32_t ret = (pc0 + 2u) & 0xFFFFu;
+          wr(0x100u | SP, ret >> 8); SP = (SP - 1u) & 0xFFu;
+          wr(0x100u | SP, ret & 0xFFu); SP = (SP - 1u) & 0xFFu;
+          wr(0x100u | SP, getP()); SP = (SP - 1u) & 0xFFu;
+          I = 1u;
+          const uint32_t lo = rd(0x1FFEu, 3u * now, 0u);
+          const uint32_t hi = rd(0x1FFFu, 3u * now, 0u);
+          nPC = lo | (hi << 8);
+        } break;
+        case K_PHA: wr(0x100u | SP, A); SP = (SP - 1u) & 0xFFu; break;
+        case K_PHP: wr(0x100u | SP, getP()); SP = (SP - 1u) & 0xFFu; break;
+        case K_PLA: {
+          const uint32_t s1 = (SP + 1u) & 0xFFu;
+          const uint32_t x = rd(0x100u | s1, 3u * now, 0u);
+          if (bad & 0x100u) goto coll;
+          SP = s1; A = x; nz(A);
+        } break;
+        case K_PLP: {
+          const uint32_t s1 = (SP + 1u) & 0xFFu;
+          const uint32_t p = rd(0x100u | s1, 3u * now, 0u);
+          if (bad & 0x100u) goto coll;
+          SP = s1;
+          nreg = p & 0x80u; V = (p >> 6) & 1u; D = (p >> 3) & 1u; I = (p >> 2) & 1u;
+          zreg = (p & 2u) ? 0u : 1u; C = p & 1u;
+        } break;
+        case K_ANC: A &= v; nz(A); C = A >> 7; break;
+        case K_ALR: { const uint32_t t = A & v; C = t & 1u; A = t >> 1; nz(A); } break;
+        case K_ARR: {
+          const uint32_t t = A & v;
+          A = (t >> 1) | (C << 7);
+          nz(A);
+          C = (A >> 6) & 1u;
+          V = ((A >> 6) ^ (A >> 5)) & 1u;
+        } break;
+        case K_SBX: { const uint32_t t = A & X; C = t >= v ? 1u : 0u; X = (t - v) & 0xFFu; nz(X); } break;
+        default:  // K_JAM: the opcode fetch happened, then the env faults, fc unchanged (R#1)
+          PC = (pc0 + 1u) & 0xFFFFu;
+          M->fault = 1u;
+          ev = SE_FAULT;
+          goto out;
+      }
+      if (d & sk::WR) wr(ea, wv);
+      (void)ff;
+      // ---- end of instruction (R#4, R#5) --------------------------------------------------
+      committed = kGenCommitted;
+      PC = nPC & 0xFFFFu;
+      pnext = now;  // phase A of the next instruction: this one's end, before any WSYNC stall
+      fc = fw != 0xFFFFFFFFu ? fw : now;
+      if (fc >= cap_cycles || xf != 0u || log_len > log_lim) {
+        if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; }  // runaway: fc / 76 >= line_cap
+        else ev = xf ? SE_FRAME : SE_LOGFULL;
+      }
+    }
+    goto out;
+  coll:  // a collision-latch read must wait for the TIA: nothing was committed
+    bank = bank0;
+    ev = SE_COLL;
+  }
+out:
+  M->PC = PC; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
+  M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
+  M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * pnext;
+  return ev | committed;
+}
+
+// Run lane 0's machine until an event; `budget` (debug) counts instructions.
+//
+// Each instruction first looks up its pre-decoded record (scalar_predecode.h) at the PC; the
+// classes it covers run a short specialised case, everything else (and every PC outside the
+// cartridge window, or rec0 == 0) falls through to the general interpreter below, which is the
+// full machine model.  Phase A of an instruction samples at the end of the previous one: that is
+// fc, except right after a WSYNC stall, which is recorded as (ws_fc, ws_now) — fc strictly
+// increases within a call, so fc == ws_fc identifies the instruction right after the stall.
+template <bool kDebug>
+__device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_t dtab0, uint32_t ram0, uint32_t lg0,
+                                            uint32_t log_lim, uint32_t cap_cycles, int32_t& budget,
+                                            uint32_t rec_all0) {
+  uint32_t PC = M->PC, A = M->A, X = M->X, Y = M->Y, SP = M->SP;
+  uint32_t C = M->C, V = M->V, D = M->D, I = M->I, nreg = M->nreg, zreg = M->zreg;
+  uint32_t fc = M->fc, bank = M->bank, log_len = M->log_len;
+  uint32_t ws_fc = fc, ws_now = M->t_phaseA / 3u;  // phase A of the first instruction
+  const uint32_t rec0 = rec_all0 + 8u * M->rom0;  // pre-decoded records of this env's ROM
+  uint32_t ev = SE_NONE;
+  // idle-loop skip (exact): the last plain timer read (PC, cycles, cycles its value holds, end)
+  uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
+  const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
+  auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
+  auto adc = [&](uint32_t m) {
+    if (!D) {
+      const uint32_t t = A + m + C;
+      V = ((~(A ^ m) & (A ^ t)) >> 7) & 1u;
+      C = t >> 8;
+      A = t & 0xFFu;
+      nz(A);
+    } else {  // NMOS decimal (R#2)
+      uint32_t lo = (A & 0xFu) + (m & 0xFu) + C;
+      if (lo >= 0xAu) lo = ((lo + 6u) & 0xFu) + 0x10u;
+      uint32_t s = (A & 0xF0u) + (m & 0xF0u) + lo;
+      const int32_t sv = (int32_t)(int8_t)(A & 0xF0u) + (int32_t)(int8_t)(m & 0xF0u) + (int32_t)lo;
+      zreg = (A + m + C) & 0xFFu;
+      nreg = s;
+      V = (sv < -128 || sv > 127) ? 1u : 0u;
+      if (s >= 0xA0u) s += 0x60u;
+      C = s >= 0x100u ? 1u : 0u;
+      A = s & 0xFFu;
+    }
+  };
+  auto sbc = [&](uint32_t m) {
+    const uint32_t t = A + (m ^ 0xFFu) + C;
+    const uint32_t r = t & 0xFFu;
+    V = ((~(A ^ (m ^ 0xFFu)) & (A ^ t)) >> 7) & 1u;
+    if (D) {  // NMOS decimal: binary flags, BCD result (R#2)
+      int32_t lo = (int32_t)(A & 0xFu) - (int32_t)(m & 0xFu) + (int32_t)C - 1;
+      if (lo < 0) lo = ((lo - 6) & 0xF) - 0x10;
+      int32_t s = (int32_t)(A & 0xF0u) - (int32_t)(m & 0xF0u) + lo;
+      if (s < 0) s -= 0x60;
+      A = (uint32_t)s & 0xFFu;
+    } else {
+      A = r;
+    }
+    C = t >> 8;
+    nz(r);
+  };
+  auto cmp = [&](uint32_t r, uint32_t m) { C = r >= m ? 1u : 0u; nz((r - m) & 0xFFu); };
   for (;;) {
     if (kDebug && budget <= 0) { ev = SE_BUDGET; break; }
     const uint32_t pc0 = PC;
@@ -394,265 +703,18 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       }
       continue;
     }
-  general : {
-    const uint32_t bank0 = bank;
-    const uint32_t pend = fc == ws_fc ? ws_now : fc;  // end cycle of the previous instruction
-    uint32_t now = fc;
-    uint32_t bad = 0u;  // bit 8 set: a collision read must wait for the TIA (abort)
-    // full bus read (phase A: T = 3 pend; phase C: T = 3 now)
-    auto rd = [&](uint32_t addr, uint32_t T, uint32_t pa) -> uint32_t {
-      const uint32_t a = addr & 0x1FFFu;
-      if (a & 0x1000u) {
-        if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
-        return ld_ro8(rom0 + (bank << 12) + (a & 0xFFFu));
-      }
-      if ((a & 0x0280u) == 0x0080u) return ld_ram(ram0 + (a & 0x7Fu));
-      const uint32_t r = s_rd_io(M, a, T, now, pa);
-      bad |= r;
-      return r & 0xFFu;
-    };
-    uint32_t op, b1, b2;
-    if ((pc0 & 0x1000u) && (pc0 & 0xFFFu) <= flim) {
-      const uint32_t p = rom0 + (bank << 12) + (pc0 & 0xFFFu);
-      op = ld_ro8(p); b1 = ld_ro8(p + 1u); b2 = ld_ro8(p + 2u);
-    } else {
-      const uint32_t f = s_fetch_slow(M, rom0, ram0, dtab0, pc0, bank, 3u * pend, now);
-      bank = f >> 25;
-      if (f & (1u << 24)) goto coll;
-      op = f & 0xFFu; b1 = (f >> 8) & 0xFFu; b2 = (f >> 16) & 0xFFu;
-    }
-    {
-      uint32_t d, e;  // decode entry (scalar_decode.h): d = mode/flags word, e = kind/aux word
-      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(d), "=r"(e) : "r"(dtab0 + 8u * op));
-      const uint32_t kind = e & 0xFFu, aux = e >> sk::AUX;
-      uint32_t n = (d >> sk::CYC) & 0xFu;
-      uint32_t nPC = pc0 + ((d >> sk::LEN) & 3u);
-      // ---- phase A: effective address ------------------------------------------------------
-      const uint32_t ix = __byte_perm(X | (Y << 8), 0u, d);  // X, Y or 0
-      uint32_t base = b1 | (b2 << 8), ea;
-      if (!(d & (sk::PTRZ | sk::PTRA))) {
-        ea = (base + ix) & ((d & sk::ZP) ? 0xFFu : 0xFFFFu);
-      } else {  // (zp,X): index before the pointer; (zp),Y: after; JMP (abs): page-wrap bug
-        const bool pa = (d & sk::PTRA) != 0u, pre = (d & sk::ZP) != 0u;
-        const uint32_t z = (b1 + (pre ? ix : 0u)) & 0xFFu;
-        const uint32_t p0 = pa ? base : z;
-        const uint32_t p1 = pa ? ((base & 0xFF00u) | ((base + 1u) & 0xFFu)) : ((z + 1u) & 0xFFu);
-        const uint32_t lo = rd(p0, 3u * pend, 1u);
-        const uint32_t hi = rd(p1, 3u * pend, 1u);
-        if (bad & 0x100u) goto coll;
-        base = lo | (hi << 8);
-        ea = (base + (pre ? 0u : ix)) & 0xFFFFu;
-      }
-      n += ((d & sk::PEN) && ((ea ^ base) & 0x100u)) ? 1u : 0u;
-      now = fc + n;
-      // ---- phase C: data read ------------------------------------------------------------
-      uint32_t v = (d & sk::ACC) ? A : b1;
-      uint32_t ff = 0u;  // timer reads: cycles over which the value read stays the same
-      if (d & sk::RD) {
-        const uint32_t a = ea & 0x1FFFu;
-        const bool cart = (a & 0x1000u) != 0u;
-        if (cart ? (a & 0xFFFu) <= hlim : (a & 0x0280u) == 0x0080u) {
-          v = cart ? ld_ro8(rom0 + (bank << 12) + (a & 0xFFFu)) : ld_ram(ram0 + (a & 0x7Fu));
-        } else if ((a & 0x1284u) == 0x0284u) {  // RIOT timer, closed form (R#24)
-          const int32_t et = (int32_t)now - M->tW;
-          const uint32_t tV = M->tV, tS = M->tS;
-          const int32_t VI = (int32_t)(tV << tS);
-          if (a & 1u) {  // TIMINT: 0 up to the expiry, 0x80 after it
-            v = et > VI ? 0x80u : 0u;
-            ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
-          } else if (et <= VI) {  // INTIM while counting: constant up to the next interval edge
-            const int32_t q = (et + (1 << tS) - 1) >> tS;
-            v = (tV - (uint32_t)q) & 0xFFu;
-            ff = (uint32_t)((q << tS) - et);
-          } else {  // INTIM after the expiry: counts down every cycle
-            v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
-          }
-        } else {
-          v = rd(a, 3u * now, 0u);
-          if (bad & 0x100u) goto coll;
-        }
-      }
-      uint32_t wv = 0u, xf = 0u;  // xf: exit flags (2 VSYNC rose); fw: cycle after a WSYNC stall
-      uint32_t fw = 0xFFFFFFFFu;
-      auto wr = [&](uint32_t addr, uint32_t val) {
-        const uint32_t a = addr & 0x1FFFu;
-        if ((a & 0x1280u) == 0x0080u) {
-          st_ram(ram0 + (a & 0x7Fu), val & 0xFFu);
-        } else if (!(a & 0x1080u)) {  // TIA: effect registers go to the log (R#4)
-          const uint32_t r = a & 0x3Fu;
-          if ((kTiaEffect >> r) & 1ull) {
-            st_log(lg0 + 4u * log_len, ((3u * now) << 14) | (r << 8) | (val & 0xFFu));
-            ++log_len;
-          } else if (r == 0x02u) {
-            fw = ((now + 75u) / 76u) * 76u;  // WSYNC: stall to the next line start (R#5)
-          } else if (r == 0x00u) {
-            xf |= s_wr_slow(M, a, val, now);
-          }
-        } else if (a & 0x1000u) {
-          if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
-        } else {
-          s_wr_slow(M, a, val, now);  // RIOT
-        }
-      };
-      // ---- operation ---------------------------------------------------------------------
-      switch (kind) {
-        case K_NOP: break;
-        case K_ORA: A |= v; nz(A); break;
-        case K_AND: A &= v; nz(A); break;
-        case K_EOR: A ^= v; nz(A); break;
-        case K_ADC: adc(v); break;
-        case K_SBC: sbc(v); break;
-        case K_CMP: cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
-        case K_BIT: nreg = v; zreg = A & v; V = (v >> 6) & 1u; break;
-        case K_LD:
-          A = (aux & 1u) ? v : A;
-          X = (aux & 2u) ? v : X;
-          Y = (aux & 4u) ? v : Y;
-          nz(v);
-          break;
-        case K_ST: wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))); break;
-        case K_ASL: C = v >> 7; wv = (v << 1) & 0xFFu; nz(wv); break;
-        case K_LSR: C = v & 1u; wv = v >> 1; nz(wv); break;
-        case K_ROL: wv = ((v << 1) | C) & 0xFFu; C = v >> 7; nz(wv); break;
-        case K_ROR: wv = (v >> 1) | (C << 7); C = v & 1u; nz(wv); break;
-        case K_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; nz(A); break;
-        case K_LSRA: C = A & 1u; A >>= 1; nz(A); break;
-        case K_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
-        case K_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
-        case K_INC: wv = (v + 1u) & 0xFFu; nz(wv); break;
-        case K_DEC: wv = (v - 1u) & 0xFFu; nz(wv); break;
-        case K_SLO: C = v >> 7; wv = (v << 1) & 0xFFu; A |= wv; nz(A); break;
-        case K_RLA: wv = ((v << 1) | C) & 0xFFu; C = v >> 7; A &= wv; nz(A); break;
-        case K_SRE: C = v & 1u; wv = v >> 1; A ^= wv; nz(A); break;
-        case K_RRA: wv = (v >> 1) | (C << 7); C = v & 1u; adc(wv); break;
-        case K_DCP: wv = (v - 1u) & 0xFFu; cmp(A, wv); break;
-        case K_ISB: wv = (v + 1u) & 0xFFu; sbc(wv); break;
-        case K_INR: {
-          const uint32_t r = (((aux & 1u) ? Y : X) + ((aux & 2u) ? 0xFFu : 1u)) & 0xFFu;
-          X = (aux & 1u) ? X : r;
-          Y = (aux & 1u) ? r : Y;
-          nz(r);
-        } break;
-        case K_TR: {
-          const uint32_t s = aux & 3u, t = (aux >> 2) & 3u;
-          const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
-          A = t == 0u ? r : A;
-          X = t == 1u ? r : X;
-          Y = t == 2u ? r : Y;
-          SP = t == 3u ? r : SP;
-          if (aux & 16u) nz(r);
-        } break;
-        case K_FLAG: {
-          const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
-          C = f == 0u ? b : C;
-          I = f == 1u ? b : I;
-          D = f == 2u ? b : D;
-          V = f == 3u ? b : V;
-        } break;
-        case K_BR: {
-          if (br_taken(aux)) {
-            const uint32_t from = nPC & 0xFFFFu;
-            const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)b1) & 0xFFFFu;
-            now += 1u + (((tgt ^ from) >> 8) & 1u);
-            nPC = tgt;
-            // idle-loop skip: [timer read; branch back to it] — later iterations whose read
-            // falls in the same constant interval repeat this one exactly, so only time
-            // advances (stopping short of the runaway cap, which the loop then reaches normally).
-            // pfe == fc: the read was the instruction right before this branch.
-            if (!kDebug && pff != 0u && pfe == fc && tgt == ppc && (pc0 & 0x1000u) && now < cap_cycles) {
-              const uint32_t P = pn + (now - fc);
-              const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
-              now += j * P;
-            }
-          }
-        } break;
-        case K_JMP: nPC = ea; break;
-        case K_JSR: {
-          const uint32_t ret = (pc0 + 2u) & 0xFFFFu;
-          wr(0x100u | SP, ret >> 8); SP = (SP - 1u) & 0xFFu;
-          wr(0x100u | SP, ret & 0xFFu); SP = (SP - 1u) & 0xFFu;
-          nPC = ea;
-        } break;
-        case K_RTS: {
-          const uint32_t s1 = (SP + 1u) & 0xFFu, s2 = (SP + 2u) & 0xFFu;
-          const uint32_t lo = rd(0x100u | s1, 3u * now, 0u);
-          const uint32_t hi = rd(0x100u | s2, 3u * now, 0u);
-          if (bad & 0x100u) goto coll;
-          SP = s2;
-          nPC = (lo | (hi << 8)) + 1u;
-        } break;
-        case K_RTI: {
-          const uint32_t s1 = (SP + 1u) & 0xFFu, s2 = (SP + 2u) & 0xFFu, s3 = (SP + 3u) & 0xFFu;
-          const uint32_t p = rd(0x100u | s1, 3u * now, 0u);
-          const uint32_t lo = rd(0x100u | s2, 3u * now, 0u);
-          const uint32_t hi = rd(0x100u | s3, 3u * now, 0u);
-          if (bad & 0x100u) goto coll;
-          SP = s3;
-          nreg = p & 0x80u; V = (p >> 6) & 1u; D = (p >> 3) & 1u; I = (p >> 2) & 1u;
-          zreg = (p & 2u) ? 0u : 1u; C = p & 1u;
-          nPC = lo | (hi << 8);
-        } break;
-        case K_BRK: {
-          const uint32_t ret = (pc0 + 2u) & 0xFFFFu;
-          wr(0x100u | SP, ret >> 8); SP = (SP - 1u) & 0xFFu;
-          wr(0x100u | SP, ret & 0xFFu); SP = (SP - 1u) & 0xFFu;
-          wr(0x100u | SP, getP()); SP = (SP - 1u) & 0xFFu;
-          I = 1u;
-          const uint32_t lo = rd(0x1FFEu, 3u * now, 0u);
-          const uint32_t hi = rd(0x1FFFu, 3u * now, 0u);
-          nPC = lo | (hi << 8);
-        } break;
-        case K_PHA: wr(0x100u | SP, A); SP = (SP - 1u) & 0xFFu; break;
-        case K_PHP: wr(0x100u | SP, getP()); SP = (SP - 1u) & 0xFFu; break;
-        case K_PLA: {
-          const uint32_t s1 = (SP + 1u) & 0xFFu;
-          const uint32_t x = rd(0x100u | s1, 3u * now, 0u);
-          if (bad & 0x100u) goto coll;
-          SP = s1; A = x; nz(A);
-        } break;
-        case K_PLP: {
-          const uint32_t s1 = (SP + 1u) & 0xFFu;
-          const uint32_t p = rd(0x100u | s1, 3u * now, 0u);
-          if (bad & 0x100u) goto coll;
-          SP = s1;
-          nreg = p & 0x80u; V = (p >> 6) & 1u; D = (p >> 3) & 1u; I = (p >> 2) & 1u;
-          zreg = (p & 2u) ? 0u : 1u; C = p & 1u;
-        } break;
-        case K_ANC: A &= v; nz(A); C = A >> 7; break;
-        case K_ALR: { const uint32_t t = A & v; C = t & 1u; A = t >> 1; nz(A); } break;
-        case K_ARR: {
-          const uint32_t t = A & v;
-          A = (t >> 1) | (C << 7);
-          nz(A);
-          C = (A >> 6) & 1u;
-          V = ((A >> 6) ^ (A >> 5)) & 1u;
-        } break;
-        case K_SBX: { const uint32_t t = A & X; C = t >= v ? 1u : 0u; X = (t - v) & 0xFFu; nz(X); } break;
-        default:  // K_JAM: the opcode fetch happened, then the env faults, fc unchanged (R#1)
-          PC = (pc0 + 1u) & 0xFFFFu;
-          M->fault = 1u;
-          ev = SE_FAULT;
-          goto out;
-      }
-      if (d & sk::WR) wr(ea, wv);
-      if (kDebug) --budget;
-      // idle-loop head candidate: plain timer read in cartridge code
-      if (d & sk::PLAIN) { pff = ff & skip_mask; ppc = pc0; pn = n; pfe = now; }
-      // ---- end of instruction (R#4, R#5) --------------------------------------------------
-      PC = nPC & 0xFFFFu;
-      if (fw != 0xFFFFFFFFu) { ws_now = now; ws_fc = fw; fc = fw; }
-      else fc = now;
-      if (fc >= cap_cycles || xf != 0u || log_len > log_lim) {
-        if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; }  // runaway: fc / 76 >= line_cap
-        else ev = xf ? SE_FRAME : SE_LOGFULL;
-        break;
-      }
-    }
-    continue;
-  coll:  // a collision-latch read must wait for the TIA: nothing was committed
-    bank = bank0;
-    ev = SE_COLL;
-    break;
+  general : {  // everything else: the general interpreter, out of line
+    M->PC = PC; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
+    M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
+    M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
+    const uint32_t r = s_gen_one(M, rom_all0, dtab0, ram0, lg0, log_lim, cap_cycles);
+    PC = M->PC; A = M->A; X = M->X; Y = M->Y; SP = M->SP;
+    C = M->C; V = M->V; D = M->D; I = M->I; nreg = M->nreg; zreg = M->zreg;
+    fc = M->fc; bank = M->bank; log_len = M->log_len;
+    ws_fc = fc; ws_now = M->t_phaseA / 3u;
+    if (kDebug && (r & kGenCommitted)) --budget;
+    ev = r & 0xFFu;
+    if (ev != SE_NONE) break;
   }
   }
 out:

@@ -24,8 +24,13 @@ __device__ __forceinline__ uint32_t with_byte(uint32_t w, int i, uint32_t v) {
 //   w0 COLUP0 COLUP1 COLUPF COLUBK | w1 PF0 PF1 PF2 CTRLPF | w2 NUSIZ0 NUSIZ1 GRP0new GRP0old
 //   w3 GRP1new GRP1old HMP0 HMP1   | w4 HMM0 HMM1 HMBL     | w5 flags(16) comb_line(16)
 //   w6 posP0 posP1 posM0 posM1     | w7 posBL, collisions(16) << 16 | t = colour clock
+// write registers that change which objects are present (PF0-2, GRP0/1, ENAM0/1, ENABL,
+// VDELP0/1, VDELBL, RESMP0/1): the pairs that could still collide are recomputed after them
+constexpr uint64_t kPresenceRegs = (7ull << 0x0D) | (0x1Full << 0x1B) | (0x1Full << 0x25);
+
 struct TiaP {
   uint32_t w0, w1, w2, w3, w4, w5, w6, w7, t;
+  uint32_t poss;  // cached possible_pairs(), 0xFFFFFFFF = stale (not kept in shared memory)
 
   __device__ __forceinline__ uint32_t f(int b) const { return (w5 >> b) & 1u; }
   __device__ __forceinline__ void setf(int b, uint32_t v) { w5 = (w5 & ~(1u << b)) | ((v & 1u) << b); }
@@ -33,6 +38,7 @@ struct TiaP {
   __device__ __forceinline__ int32_t comb_line() const { return (int32_t)(int16_t)(w5 >> 16); }
   __device__ __forceinline__ void load(const uint32_t* tw) {
     w0 = tw[0]; w1 = tw[1]; w2 = tw[2]; w3 = tw[3]; w4 = tw[4]; w5 = tw[5]; w6 = tw[6]; w7 = tw[7]; t = tw[8];
+    poss = 0xFFFFFFFFu;
   }
   __device__ __forceinline__ void store(uint32_t* tw) const {
     tw[0] = w0; tw[1] = w1; tw[2] = w2; tw[3] = w3; tw[4] = w4; tw[5] = w5; tw[6] = w6; tw[7] = w7; tw[8] = t;
@@ -42,7 +48,11 @@ struct TiaP {
   __device__ __forceinline__ uint32_t ball_on() const { return f(9) ? f(6) : f(5); }
 
   // collision latches the objects present now could still set (an absent object cannot collide)
-  __device__ __forceinline__ uint32_t open_pairs() const {
+  __device__ __forceinline__ uint32_t open_pairs() {
+    if (poss == 0xFFFFFFFFu) poss = possible_pairs();
+    return poss & ~coll();
+  }
+  __device__ __forceinline__ uint32_t possible_pairs() const {
     const uint32_t p0 = grp0() != 0u, p1 = grp1() != 0u;
     const uint32_t m0 = f(3) & (f(10) ^ 1u), m1 = f(4) & (f(11) ^ 1u);
     const uint32_t bl = ball_on();
@@ -51,7 +61,7 @@ struct TiaP {
                               ((p0 & pf) << 4) | ((p0 & bl) << 5) | ((p1 & pf) << 6) | ((p1 & bl) << 7) |
                               ((m0 & pf) << 8) | ((m0 & bl) << 9) | ((m1 & pf) << 10) | ((m1 & bl) << 11) |
                               ((bl & pf) << 12) | ((p0 & p1) << 14) | ((m0 & m1) << 15);
-    return possible & ~coll();
+    return possible;
   }
 
   // apply a logged write at colour clock T (DESIGN.md §2 R#7-R#12)
@@ -114,6 +124,7 @@ struct TiaP {
       case 0x2C: w7 &= 0xFFFFu; break;               // CXCLR
       default: break;
     }
+    if ((kPresenceRegs >> r) & 1ull) poss = 0xFFFFFFFFu;
   }
 };
 
@@ -228,6 +239,10 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   const uint32_t t0 = t.t;
   if (t_to <= t0) return;
   t.t = t_to;
+  const bool vblank = t.f(0) != 0u;
+  // frames that are not rendered only need collisions: nothing to do under VBLANK or when no
+  // pair that is still unlatched can collide (cached until a presence register changes)
+  if (!rb.render && (vblank || t.open_pairs() == 0u)) return;
   const uint32_t l0 = t0 / 228u, l1 = (t_to - 1) / 228u;
   const uint32_t h0 = t0 - l0 * 228u, h1 = t_to - l1 * 228u;
   const uint32_t xa0 = h0 > 68u ? h0 - 68u : 0u;
@@ -235,10 +250,9 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   // a span inside one line with no visible clock (e.g. writes right after WSYNC, in HBLANK)
   // neither collides nor draws, and cannot complete a row (that needs xb1 = 160 > xa0)
   if (l1 == l0 && xb1 <= xa0) return;
-  const bool vblank = t.f(0) != 0u;
-  const bool need_coll = !vblank && t.open_pairs() != 0u;
   const uint32_t w0 = ystart, w1 = ystart + (uint32_t)kFrameH;
   const bool any_win = rb.render && l1 >= w0 && l0 < w1;
+  const bool need_coll = !vblank && t.open_pairs() != 0u;
   if (!need_coll && !any_win) return;
   Words w{0u, 0u, 0u, 0u, 0u, 0u};
   if (!vblank) w = object_words(t, lane < 10u ? (lane >> 1) : 0u);
