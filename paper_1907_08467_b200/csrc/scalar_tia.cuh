@@ -28,6 +28,40 @@ __device__ __forceinline__ uint32_t with_byte(uint32_t w, int i, uint32_t v) {
 // VDELP0/1, VDELBL, RESMP0/1): the pairs that could still collide are recomputed after them
 constexpr uint64_t kPresenceRegs = (7ull << 0x0D) | (0x1Full << 0x1B) | (0x1Full << 0x25);
 
+// collision pairs two present objects can set, by presence bits (0 P0, 1 P1, 2 M0, 3 M1, 4 BL,
+// 5 PF) -> latch bits (bit 2r = D7, 2r+1 = D6 of read register r: CXM0P M0-P1/M0-P0, CXM1P
+// M1-P0/M1-P1, CXP0FB P0-PF/P0-BL, CXP1FB P1-PF/P1-BL, CXM0FB M0-PF/M0-BL, CXM1FB M1-PF/M1-BL,
+// CXBLPF BL-PF, CXPPMM P0-P1/M0-M1)
+struct PairTable {
+  uint16_t v[64];
+  constexpr PairTable() : v() {
+    for (int i = 0; i < 64; ++i) {
+      const int p0 = i & 1, p1 = (i >> 1) & 1, m0 = (i >> 2) & 1, m1 = (i >> 3) & 1, bl = (i >> 4) & 1,
+                pf = (i >> 5) & 1;
+      v[i] = (uint16_t)((m0 & p1) | ((m0 & p0) << 1) | ((m1 & p0) << 2) | ((m1 & p1) << 3) | ((p0 & pf) << 4) |
+                        ((p0 & bl) << 5) | ((p1 & pf) << 6) | ((p1 & bl) << 7) | ((m0 & pf) << 8) |
+                        ((m0 & bl) << 9) | ((m1 & pf) << 10) | ((m1 & bl) << 11) | ((bl & pf) << 12) |
+                        ((p0 & p1) << 14) | ((m0 & m1) << 15));
+    }
+  }
+};
+__constant__ PairTable kPairTable = PairTable();
+
+// objects whose coverage words a register write changes (bits 0 P0, 1 P1, 2 M0, 3 M1, 4 BL,
+// 5 PF): NUSIZ, CTRLPF, REFP, PF0-2, RESxx, GRP0/1 (and the VDEL copies), ENAx, VDELxx, RESMPx,
+// HMOVE.  Colours, VBLANK, HMxx, HMCLR and CXCLR change none.
+struct DirtyTable {
+  uint8_t v[64];
+  constexpr DirtyTable() : v() {
+    v[0x04] = 1 | 4; v[0x05] = 2 | 8; v[0x0A] = 16 | 32; v[0x0B] = 1; v[0x0C] = 2;
+    v[0x0D] = v[0x0E] = v[0x0F] = 32;
+    v[0x10] = 1; v[0x11] = 2; v[0x12] = 4; v[0x13] = 8; v[0x14] = 16;
+    v[0x1B] = 1 | 2; v[0x1C] = 1 | 2 | 16; v[0x1D] = 4; v[0x1E] = 8; v[0x1F] = 16;
+    v[0x25] = 1; v[0x26] = 2; v[0x27] = 16; v[0x28] = 4; v[0x29] = 8; v[0x2A] = 1 | 2 | 4 | 8 | 16;
+  }
+};
+__constant__ DirtyTable kDirtyTable = DirtyTable();
+
 struct TiaP {
   uint32_t w0, w1, w2, w3, w4, w5, w6, w7, t;
   uint32_t poss;  // cached possible_pairs(), 0xFFFFFFFF = stale (not kept in shared memory)
@@ -57,17 +91,11 @@ struct TiaP {
     const uint32_t m0 = f(3) & (f(10) ^ 1u), m1 = f(4) & (f(11) ^ 1u);
     const uint32_t bl = ball_on();
     const uint32_t pf = (w1 & 0x00FFFFF0u) != 0u;  // PF0 D4-D7, PF1, PF2
-    const uint32_t possible = (m0 & p1) | ((m0 & p0) << 1) | ((m1 & p0) << 2) | ((m1 & p1) << 3) |
-                              ((p0 & pf) << 4) | ((p0 & bl) << 5) | ((p1 & pf) << 6) | ((p1 & bl) << 7) |
-                              ((m0 & pf) << 8) | ((m0 & bl) << 9) | ((m1 & pf) << 10) | ((m1 & bl) << 11) |
-                              ((bl & pf) << 12) | ((p0 & p1) << 14) | ((m0 & m1) << 15);
-    return possible;
+    return kPairTable.v[p0 | (p1 << 1) | (m0 << 2) | (m1 << 3) | (bl << 4) | (pf << 5)];
   }
 
   // apply a logged write at colour clock T (DESIGN.md §2 R#7-R#12)
   __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T) {
-    const uint32_t line = T / 228u, h = T - line * 228u;
-    const int32_t hp = (int32_t)h - 68;
     switch (r) {
       case 0x01: setf(0, v >> 1); break;
       case 0x04: w2 = with_byte(w2, 0, v); break;
@@ -78,6 +106,7 @@ struct TiaP {
       case 0x0C: setf(2, v >> 3); break;
       case 0x0D: case 0x0E: case 0x0F: w1 = with_byte(w1, (int)(r - 0x0Du), v); break;
       case 0x10: case 0x11: case 0x12: case 0x13: case 0x14: {  // RESP0/1, RESM0/1, RESBL
+        const int32_t hp = (int32_t)(T % 228u) - 68;
         const uint32_t base = r <= 0x11u ? 5u : 4u;
         const uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
         if (r == 0x14u) w7 = with_byte(w7, 0, p);
@@ -118,6 +147,7 @@ struct TiaP {
         const uint32_t m0 = mv(byte_of(w6, 2), byte_of(w4, 0)), m1 = mv(byte_of(w6, 3), byte_of(w4, 1));
         w6 = p0 | (p1 << 8) | (m0 << 16) | (m1 << 24);
         w7 = with_byte(w7, 0, mv(byte_of(w7, 0), byte_of(w4, 2)));
+        const uint32_t line = T / 228u, h = T - line * 228u;
         if (h < 68u) w5 = (w5 & 0xFFFFu) | ((line & 0xFFFFu) << 16);
       } break;
       case 0x2B: w3 &= 0x0000FFFFu; w4 = 0u; break;  // HMCLR
@@ -162,19 +192,21 @@ __device__ __forceinline__ uint32_t missile_word(uint32_t k, uint32_t pos, uint3
   return obj_word(k, pat, pos, (mode == 5u || mode == 7u) ? 1u : Tia::copies(mode));
 }
 
-__device__ __forceinline__ Words object_words(const TiaP& t, uint32_t k) {
-  Words w;
-  w.p0 = player_word(k, byte_of(t.w6, 0), byte_of(t.w2, 0), t.grp0(), t.f(1));
-  w.p1 = player_word(k, byte_of(t.w6, 1), byte_of(t.w2, 1), t.grp1(), t.f(2));
-  w.m0 = missile_word(k, byte_of(t.w6, 2), byte_of(t.w2, 0), t.f(3) && !t.f(10));
-  w.m1 = missile_word(k, byte_of(t.w6, 3), byte_of(t.w2, 1), t.f(4) && !t.f(11));
-  w.bl = t.ball_on() ? obj_word(k, (1u << (1u << ((byte_of(t.w1, 3) >> 4) & 3u))) - 1u, byte_of(t.w7, 0), 1u) : 0u;
-  // playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), each 4 pixels wide
-  const uint32_t left = ((byte_of(t.w1, 0) >> 4) & 0xFu) | (rev8(byte_of(t.w1, 1)) << 4) | (byte_of(t.w1, 2) << 12);
-  const uint32_t right = (t.w1 & 0x01000000u) ? (__brev(left) >> 12) : left;
-  const uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
-  w.pf = spread4((uint32_t)(cells >> (8u * k)));
-  return w;
+// coverage words of the six objects in the lane's word k, recomputed only for the objects
+// flagged in `dirty`; playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), 4 px each
+__device__ __forceinline__ void update_words(const TiaP& t, uint32_t k, Words& w, uint32_t dirty) {
+  if (dirty & 1u) w.p0 = player_word(k, byte_of(t.w6, 0), byte_of(t.w2, 0), t.grp0(), t.f(1));
+  if (dirty & 2u) w.p1 = player_word(k, byte_of(t.w6, 1), byte_of(t.w2, 1), t.grp1(), t.f(2));
+  if (dirty & 4u) w.m0 = missile_word(k, byte_of(t.w6, 2), byte_of(t.w2, 0), t.f(3) && !t.f(10));
+  if (dirty & 8u) w.m1 = missile_word(k, byte_of(t.w6, 3), byte_of(t.w2, 1), t.f(4) && !t.f(11));
+  if (dirty & 16u)
+    w.bl = t.ball_on() ? obj_word(k, (1u << (1u << ((byte_of(t.w1, 3) >> 4) & 3u))) - 1u, byte_of(t.w7, 0), 1u) : 0u;
+  if (dirty & 32u) {
+    const uint32_t left = ((byte_of(t.w1, 0) >> 4) & 0xFu) | (rev8(byte_of(t.w1, 1)) << 4) | (byte_of(t.w1, 2) << 12);
+    const uint32_t right = (t.w1 & 0x01000000u) ? (__brev(left) >> 12) : left;
+    const uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
+    w.pf = spread4((uint32_t)(cells >> (8u * k)));
+  }
 }
 
 // the row being assembled: lane j < 10 holds chunk j (pixels 16j..16j+15)
@@ -235,7 +267,7 @@ __device__ __forceinline__ void row_done(RowBuf& rb, uint32_t lane) {
 
 // advance the warp-uniform TIA over colour clocks [t.t, t_to)
 __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb, uint32_t lane, uint32_t ystart,
-                                              const uint8_t* gray) {
+                                              const uint8_t* gray, Words& w, uint32_t& dirty) {
   const uint32_t t0 = t.t;
   if (t_to <= t0) return;
   t.t = t_to;
@@ -254,8 +286,12 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   const bool any_win = rb.render && l1 >= w0 && l0 < w1;
   const bool need_coll = !vblank && t.open_pairs() != 0u;
   if (!need_coll && !any_win) return;
-  Words w{0u, 0u, 0u, 0u, 0u, 0u};
-  if (!vblank) w = object_words(t, lane < 10u ? (lane >> 1) : 0u);
+  // coverage words of the lane's 32-pixel word, recomputed only for objects whose registers
+  // changed since (under VBLANK no object is drawn and no pair collides: the words are unused)
+  if (!vblank && dirty) {
+    update_words(t, lane < 10u ? (lane >> 1) : 0u, w, dirty);
+    dirty = 0u;
+  }
   if (need_coll) {  // collisions depend on x only: the union of the span's visible x ranges
     uint32_t bits;
     if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) {
@@ -300,13 +336,16 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
                                                const uint8_t* gray) {
   TiaP t;
   t.load(tw);
+  Words w{0u, 0u, 0u, 0u, 0u, 0u};
+  uint32_t dirty = 0x3Fu;
   for (uint32_t k = 0; k < n; ++k) {
     const uint32_t e = lg[k];
-    const uint32_t T = e >> 14;
-    catch_up_coop(t, T, rb, lane, ystart, gray);
-    t.apply((e >> 8) & 0x3Fu, e & 0xFFu, T);
+    const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
+    catch_up_coop(t, T, rb, lane, ystart, gray, w, dirty);
+    t.apply(r, e & 0xFFu, T);
+    dirty |= kDirtyTable.v[r];
   }
-  if (fin) catch_up_coop(t, t_final, rb, lane, ystart, gray);
+  if (fin) catch_up_coop(t, t_final, rb, lane, ystart, gray, w, dirty);
   __syncwarp();
   if (lane == 0u) t.store(tw);
   __syncwarp();
