@@ -474,23 +474,27 @@ out:
 
 // Run lane 0's machine until an event; `budget` (debug) counts instructions.
 //
-// Each instruction first looks up its pre-decoded record (scalar_predecode.h) at the PC; the
-// classes it covers run a short specialised case, everything else (and every PC outside the
-// cartridge window, or rec0 == 0) falls through to the general interpreter below, which is the
-// full machine model.  Phase A of an instruction samples at the end of the previous one: that is
-// fc, except right after a WSYNC stall, which is recorded as (ws_fc, ws_now) — fc strictly
-// increases within a call, so fc == ws_fc identifies the instruction right after the stall.
+// Every instruction whose pre-decoded record (scalar_predecode.h) has a fast class runs a short
+// specialised case; everything else goes through s_gen_one().  While in the fast loop the PC is
+// in a cartridge window and is kept split: pcw = PC & 0xF000, pco = PC & 0xFFF (fast classes
+// never leave the window except C_JMP, which sets both; the general path re-enters the fast loop
+// only with PC in a cartridge window).  Phase A of an instruction samples at the end of the
+// previous one: that is fc, except right after a WSYNC stall, recorded as (ws_fc, ws_now) — fc
+// strictly increases within a call, so fc == ws_fc identifies the instruction after the stall.
 template <bool kDebug>
 __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_t dtab0, uint32_t ram0, uint32_t lg0,
                                             uint32_t log_lim, uint32_t cap_cycles, int32_t& budget,
                                             uint32_t rec_all0) {
-  uint32_t PC = M->PC, A = M->A, X = M->X, Y = M->Y, SP = M->SP;
+  uint32_t A = M->A, X = M->X, Y = M->Y, SP = M->SP;
   uint32_t C = M->C, V = M->V, D = M->D, I = M->I, nreg = M->nreg, zreg = M->zreg;
   uint32_t fc = M->fc, bank = M->bank, log_len = M->log_len;
+  uint32_t pcw = M->PC & 0xF000u, pco = M->PC & 0xFFFu;
   uint32_t ws_fc = fc, ws_now = M->t_phaseA / 3u;  // phase A of the first instruction
   const uint32_t rec0 = rec_all0 + 8u * M->rom0;  // pre-decoded records of this env's ROM
+  const uint32_t rom0 = rom_all0 + M->rom0;       // its raw image (data reads)
+  uint32_t recb = rec0 + (bank << 15), romb = rom0 + (bank << 12);
   uint32_t ev = SE_NONE;
-  // idle-loop skip (exact): the last plain timer read (PC, cycles, cycles its value holds, end)
+  // idle-loop skip (exact): the last plain timer read (offset, cycles, cycles its value holds, end)
   uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
   const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
   auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
@@ -531,27 +535,26 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
     nz(r);
   };
   auto cmp = [&](uint32_t r, uint32_t m) { C = r >= m ? 1u : 0u; nz((r - m) & 0xFFu); };
+  if (kDebug && budget <= 0) { ev = SE_BUDGET; goto out; }
+  if (!(pcw & 0x1000u)) goto general;  // entered outside the cartridge (code in RAM)
   for (;;) {
     if (kDebug && budget <= 0) { ev = SE_BUDGET; break; }
-    const uint32_t pc0 = PC;
     {
-      // ---- fast path: pre-decoded record -------------------------------------------------
       uint32_t lo, hi;
-      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec0 + (((bank << 12) | (pc0 & 0xFFFu)) << 3)));
-      const uint32_t cls = (pc0 & 0x1000u) ? (lo >> pd::CLS) & 31u : (uint32_t)C_GEN;
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(recb + 8u * pco));
+      const uint32_t cls = lo & 31u;
       uint32_t now = fc + ((lo >> pd::CYC) & 0xFu);
-      uint32_t nPC = pc0 + ((lo >> pd::LEN) & 3u);
-      const uint32_t aux = (lo >> pd::AUX) & 7u;
-      const uint32_t opnd = hi & 0xFFFFu;
+      uint32_t npco = lo >> pd::NXT;
       if (cls == C_BR) {  // the most frequent class, tested before the switch
+        const uint32_t aux = lo >> pd::AUX;
         const uint32_t src = (aux & 2u) ? ((aux & 1u) ? zreg : C) : ((aux & 1u) ? V : nreg);
-        if (((src & (lo >> pd::REG)) != 0u) == ((aux & 4u) != 0u)) {
-          const uint32_t from = nPC & 0xFFFFu;
-          const uint32_t tgt = (from + (uint32_t)(int32_t)(int8_t)opnd) & 0xFFFFu;
-          now += 1u + (((tgt ^ from) >> 8) & 1u);
-          nPC = tgt;
-          // idle-loop skip: [timer read; branch back to it] (see the general path)
-          if (!kDebug && pff != 0u && pfe == fc && tgt == ppc && now < cap_cycles) {
+        if (((src & (hi >> 16)) != 0u) == ((aux & 4u) != 0u)) {
+          npco = hi & 0xFFFu;
+          // idle-loop skip: [timer read; branch back to it] — later iterations whose read falls
+          // in the same constant interval repeat this one exactly, so only time advances
+          // (stopping short of the runaway cap, which the loop then reaches normally).
+          // pfe == fc: the read was the instruction right before this branch.
+          if (!kDebug && pff != 0u && pfe == fc && npco == ppc && now < cap_cycles) {
             const uint32_t P = pn + (now - fc);
             const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
             now += j * P;
@@ -560,142 +563,146 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           // the step kernel checks the cap there (a faulted env's state is replaced by the
           // reset cache, so only the step of the fault matters); the debug entry checks it
           // after every instruction
-          if (!kDebug && now >= cap_cycles) { PC = nPC; fc = now; M->fault = 2u; ev = SE_FAULT; break; }
+          if (!kDebug && now >= cap_cycles) { pco = npco; fc = now; M->fault = 2u; ev = SE_FAULT; break; }
+        } else {
+          now = fc + 2u;
         }
         goto fast_done;
       }
       {
-      // data operand: RAM[(opnd + ix) & 0x7F] (zero page: bit 7 of opnd + ix selects RAM, else
-      // the general path) or the cartridge byte (opnd + ix) & 0xFFF of the bank (page-cross +1)
-      const uint32_t t = opnd + __byte_perm(X | (Y << 8), 0u, hi >> 16);
-      uint32_t v = 0u;
-      auto rd_operand = [&]() -> bool {
-        if (lo & pd::RAM) {
-          if (!(t & 0x80u)) return false;
-          v = ld_ram(ram0 + (t & 0x7Fu));
-        } else {
-          v = ld_ro8(rec0 + (((bank << 12) | (t & 0xFFFu)) << 3));
-        }
-        now += (lo & pd::PEN) ? ((t ^ opnd) >> 8) & 1u : 0u;
-        return true;
-      };
-      auto ram_addr = [&]() -> bool { return (t & 0x80u) != 0u; };
-      switch (cls) {
-        case C_ORA: if (!rd_operand()) goto general; A |= v; nz(A); break;
-        case C_AND: if (!rd_operand()) goto general; A &= v; nz(A); break;
-        case C_EOR: if (!rd_operand()) goto general; A ^= v; nz(A); break;
-        case C_ADC: if (!rd_operand()) goto general; adc(v); break;
-        case C_SBC: if (!rd_operand()) goto general; sbc(v); break;
-        case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
-        case C_BIT: if (!rd_operand()) goto general; nreg = v; zreg = A & v; V = (v >> 6) & 1u; break;
-        case C_LD:
-          if (!rd_operand()) goto general;
-          A = (aux & 1u) ? v : A;
-          X = (aux & 2u) ? v : X;
-          Y = (aux & 4u) ? v : Y;
-          nz(v);
-          break;
-        case C_NOPR: if (!rd_operand()) goto general; break;
-        case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
-          const int32_t et = (int32_t)now - M->tW;
-          const uint32_t tV = M->tV, tS = M->tS;
-          const int32_t VI = (int32_t)(tV << tS);
-          uint32_t ff = 0u;
-          if (opnd & 1u) {
-            v = et > VI ? 0x80u : 0u;
-            ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
-          } else if (et <= VI) {
-            const int32_t q = (et + (1 << tS) - 1) >> tS;
-            v = (tV - (uint32_t)q) & 0xFFu;
-            ff = (uint32_t)((q << tS) - et);
+        const uint32_t aux = (lo >> pd::AUX) & 7u;
+        // data operand: RAM[(opnd + ix) & 0x7F] (needs bit 7 of opnd + ix, else the general
+        // path: zp,X into the TIA) or the cartridge byte (opnd + ix) & 0xFFF of the bank
+        const uint32_t opnd = hi >> pd::OPND;
+        const uint32_t t = opnd + __byte_perm(X | (Y << 8), 0u, hi);
+        uint32_t v = 0u;
+        auto rd_operand = [&]() -> bool {
+          if (hi & pd::RAM) {
+            if (!(t & 0x80u)) return false;
+            v = ld_ram(ram0 + (t & 0x7Fu));
           } else {
-            v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
+            v = ld_ro8(romb + (t & 0xFFFu));
           }
-          if (cls == C_TLD) {
+          now += (hi & pd::PEN) ? ((t ^ opnd) >> 8) & 1u : 0u;
+          return true;
+        };
+        switch (cls) {
+          case C_ORA: if (!rd_operand()) goto general; A |= v; nz(A); break;
+          case C_AND: if (!rd_operand()) goto general; A &= v; nz(A); break;
+          case C_EOR: if (!rd_operand()) goto general; A ^= v; nz(A); break;
+          case C_ADC: if (!rd_operand()) goto general; adc(v); break;
+          case C_SBC: if (!rd_operand()) goto general; sbc(v); break;
+          case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
+          case C_BIT: if (!rd_operand()) goto general; nreg = v; zreg = A & v; V = (v >> 6) & 1u; break;
+          case C_LD:
+            if (!rd_operand()) goto general;
             A = (aux & 1u) ? v : A;
             X = (aux & 2u) ? v : X;
             Y = (aux & 4u) ? v : Y;
             nz(v);
-          } else {
-            nreg = v; zreg = A & v; V = (v >> 6) & 1u;
-          }
-          pff = ff & skip_mask;
-          ppc = pc0;
-          pn = now - fc;
-          pfe = now;
-        } break;
-        case C_STRAM:
-          if (!ram_addr()) goto general;
-          st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
-          break;
-        case C_STTIA: {
-          const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
-          st_log(lg0 + 4u * log_len, ((3u * now) << 14) | ((lo >> pd::REG) << 8) | wv);
-          ++log_len;
-          if (log_len > log_lim) {
-            PC = nPC & 0xFFFFu;
-            fc = now;
-            if (kDebug) --budget;
-            if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; }
-            else ev = SE_LOGFULL;
-            goto out;
-          }
-        } break;
-        case C_WSYNC:  // stall to the next line start (R#5)
-          ws_now = now;
-          now = ((now + 75u) / 76u) * 76u;
-          ws_fc = now;
-          break;
-        case C_INC: case C_DEC: case C_ASL: case C_LSR: case C_ROL: case C_ROR: {
-          if (!ram_addr()) goto general;
-          const uint32_t a = ram0 + (t & 0x7Fu);
-          const uint32_t m = ld_ram(a);
-          uint32_t r;
-          if (cls == C_INC) r = (m + 1u) & 0xFFu;
-          else if (cls == C_DEC) r = (m - 1u) & 0xFFu;
-          else if (cls == C_ASL) { C = m >> 7; r = (m << 1) & 0xFFu; }
-          else if (cls == C_LSR) { C = m & 1u; r = m >> 1; }
-          else if (cls == C_ROL) { r = ((m << 1) | C) & 0xFFu; C = m >> 7; }
-          else { r = (m >> 1) | (C << 7); C = m & 1u; }
-          nz(r);
-          st_ram(a, r);
-        } break;
-        case C_INR: {
-          const uint32_t r = (((aux & 1u) ? Y : X) + ((aux & 2u) ? 0xFFu : 1u)) & 0xFFu;
-          X = (aux & 1u) ? X : r;
-          Y = (aux & 1u) ? r : Y;
-          nz(r);
-        } break;
-        case C_TR: {
-          const uint32_t s = aux & 3u, d = lo >> pd::REG;
-          const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
-          A = d == 0u ? r : A;
-          X = d == 1u ? r : X;
-          Y = d == 2u ? r : Y;
-          SP = d == 3u ? r : SP;
-          if (aux & 4u) nz(r);
-        } break;
-        case C_FLAG: {
-          const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
-          C = f == 0u ? b : C;
-          I = f == 1u ? b : I;
-          D = f == 2u ? b : D;
-          V = f == 3u ? b : V;
-        } break;
-        case C_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; nz(A); break;
-        case C_LSRA: C = A & 1u; A >>= 1; nz(A); break;
-        case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
-        case C_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
-        case C_NOP: break;
-        case C_JMP:
-          nPC = opnd;
-          if (!kDebug && now >= cap_cycles) { PC = nPC; fc = now; M->fault = 2u; ev = SE_FAULT; goto out; }
-          break;
-        default: goto general;
-      }
+            break;
+          case C_NOPR: if (!rd_operand()) goto general; break;
+          case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
+            const int32_t et = (int32_t)now - M->tW;
+            const uint32_t tV = M->tV, tS = M->tS;
+            const int32_t VI = (int32_t)(tV << tS);
+            uint32_t ff = 0u;
+            if (hi & 1u) {  // TIMINT
+              v = et > VI ? 0x80u : 0u;
+              ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
+            } else if (et <= VI) {
+              const int32_t q = (et + (1 << tS) - 1) >> tS;
+              v = (tV - (uint32_t)q) & 0xFFu;
+              ff = (uint32_t)((q << tS) - et);
+            } else {
+              v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
+            }
+            if (cls == C_TLD) {
+              A = (aux & 1u) ? v : A;
+              X = (aux & 2u) ? v : X;
+              Y = (aux & 4u) ? v : Y;
+              nz(v);
+            } else {
+              nreg = v; zreg = A & v; V = (v >> 6) & 1u;
+            }
+            pff = ff & skip_mask;
+            ppc = pco;
+            pn = now - fc;
+            pfe = now;
+          } break;
+          case C_STRAM:
+            if (!(t & 0x80u)) goto general;
+            st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
+            break;
+          case C_STTIA: {
+            const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
+            st_log(lg0 + 4u * log_len, ((3u * now) << 14) | hi | wv);
+            ++log_len;
+            if (log_len > log_lim) {
+              pco = npco;
+              fc = now;
+              if (kDebug) --budget;
+              if (fc >= cap_cycles) { M->fault = 2u; ev = SE_FAULT; }
+              else ev = SE_LOGFULL;
+              goto out;
+            }
+          } break;
+          case C_WSYNC:  // stall to the next line start (R#5)
+            ws_now = now;
+            now = ((now + 75u) / 76u) * 76u;
+            ws_fc = now;
+            break;
+          case C_INC: case C_DEC: case C_ASL: case C_LSR: case C_ROL: case C_ROR: {
+            if (!(t & 0x80u)) goto general;
+            const uint32_t a = ram0 + (t & 0x7Fu);
+            const uint32_t m = ld_ram(a);
+            uint32_t r;
+            if (cls == C_INC) r = (m + 1u) & 0xFFu;
+            else if (cls == C_DEC) r = (m - 1u) & 0xFFu;
+            else if (cls == C_ASL) { C = m >> 7; r = (m << 1) & 0xFFu; }
+            else if (cls == C_LSR) { C = m & 1u; r = m >> 1; }
+            else if (cls == C_ROL) { r = ((m << 1) | C) & 0xFFu; C = m >> 7; }
+            else { r = (m >> 1) | (C << 7); C = m & 1u; }
+            nz(r);
+            st_ram(a, r);
+          } break;
+          case C_INR: {
+            const uint32_t r = (((aux & 1u) ? Y : X) + ((aux & 2u) ? 0xFFu : 1u)) & 0xFFu;
+            X = (aux & 1u) ? X : r;
+            Y = (aux & 1u) ? r : Y;
+            nz(r);
+          } break;
+          case C_TR: {
+            const uint32_t s = aux & 3u, d = hi;
+            const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
+            A = d == 0u ? r : A;
+            X = d == 1u ? r : X;
+            Y = d == 2u ? r : Y;
+            SP = d == 3u ? r : SP;
+            if (aux & 4u) nz(r);
+          } break;
+          case C_FLAG: {
+            const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
+            C = f == 0u ? b : C;
+            I = f == 1u ? b : I;
+            D = f == 2u ? b : D;
+            V = f == 3u ? b : V;
+          } break;
+          case C_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; nz(A); break;
+          case C_LSRA: C = A & 1u; A >>= 1; nz(A); break;
+          case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
+          case C_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
+          case C_NOP: break;
+          case C_JMP:
+            pcw = hi & 0xF000u;
+            npco = hi & 0xFFFu;
+            if (!kDebug && now >= cap_cycles) { pco = npco; fc = now; M->fault = 2u; ev = SE_FAULT; goto out; }
+            break;
+          default: goto general;
+        }
       }
     fast_done:
-      PC = nPC & 0xFFFFu;
+      pco = npco;
       fc = now;
       if (kDebug) {
         --budget;
@@ -703,22 +710,30 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       }
       continue;
     }
-  general : {  // everything else: the general interpreter, out of line
-    M->PC = PC; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
-    M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
-    M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
-    const uint32_t r = s_gen_one(M, rom_all0, dtab0, ram0, lg0, log_lim, cap_cycles);
-    PC = M->PC; A = M->A; X = M->X; Y = M->Y; SP = M->SP;
-    C = M->C; V = M->V; D = M->D; I = M->I; nreg = M->nreg; zreg = M->zreg;
-    fc = M->fc; bank = M->bank; log_len = M->log_len;
-    ws_fc = fc; ws_now = M->t_phaseA / 3u;
-    if (kDebug && (r & kGenCommitted)) --budget;
-    ev = r & 0xFFu;
-    if (ev != SE_NONE) break;
-  }
+  general:  // everything else: the general interpreter, out of line, until the PC is back in a
+            // cartridge window
+    for (;;) {
+      M->PC = pcw | pco; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
+      M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
+      M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
+      const uint32_t r = s_gen_one(M, rom_all0, dtab0, ram0, lg0, log_lim, cap_cycles);
+      const uint32_t PC = M->PC;
+      pcw = PC & 0xF000u; pco = PC & 0xFFFu;
+      A = M->A; X = M->X; Y = M->Y; SP = M->SP;
+      C = M->C; V = M->V; D = M->D; I = M->I; nreg = M->nreg; zreg = M->zreg;
+      fc = M->fc; bank = M->bank; log_len = M->log_len;
+      ws_fc = fc; ws_now = M->t_phaseA / 3u;
+      if (kDebug && (r & kGenCommitted)) --budget;
+      ev = r & 0xFFu;
+      if (ev != SE_NONE) goto out;
+      if (PC & 0x1000u) break;
+      if (kDebug && budget <= 0) { ev = SE_BUDGET; goto out; }
+    }
+    recb = rec0 + (bank << 15);
+    romb = rom0 + (bank << 12);
   }
 out:
-  M->PC = PC; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
+  M->PC = pcw | pco; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
   M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
   M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
   return ev;

@@ -4,9 +4,9 @@
 // every byte offset of every 4 KB bank can be decoded once, at cule_create, as if an instruction
 // started there.  One 8-byte record per ROM byte holds everything the interpreter needs to run
 // that instruction without touching the decode table: the operation class (one case of the
-// fast-path switch), length, base cycles, page-cross rule, register selector, the operand and
-// the index selector.  Byte 0 of the record is the ROM byte itself, so data reads from the
-// cartridge (tables, immediates) read the record array.
+// fast-path switch), base cycles, the fall-through PC, page-cross rule, register selector, the
+// operand and the index selector — laid out so that the fields every instruction needs come out
+// of the record in one or two integer operations.
 //
 // The class also folds in what the address alone decides: a direct (zero-page or absolute)
 // operand is statically RAM, cartridge, TIA or RIOT, so the fast path never decodes the bus for
@@ -24,15 +24,18 @@
 namespace cule {
 
 namespace pd {
-// record word lo
-constexpr uint32_t CLS = 8;     // 5 bits: class
-constexpr uint32_t LEN = 13;    // 2 bits
-constexpr uint32_t CYC = 15;    // 4 bits: base cycles
-constexpr uint32_t PEN = 1u << 19;  // +1 cycle when the indexed address crosses a page
-constexpr uint32_t AUX = 20;    // 3 bits: register selector (see classes)
-constexpr uint32_t RAM = 1u << 23;  // the operand addresses RAM (else the cartridge)
-constexpr uint32_t REG = 24;    // 8 bits: TIA register (C_STTIA)
-// record word hi: bits 0-15 operand, bits 16-31 index byte-permute selector (sk::SEL_*)
+// Record word lo: [0:5) class, [5:8) aux, [8:12) base cycles (C_BR: cycles when taken),
+// [20:32) low 12 bits of the fall-through PC (the instruction ends inside the 4 KB window).
+constexpr uint32_t AUX = 5, CYC = 8, NXT = 20;
+// Record word hi, by class:
+//   reads / stores / read-modify-writes: [0:16) byte-permute selector of the index (sk::SEL_*),
+//     [16:28) operand (RAM: zero-page address; cartridge: offset in the bank, immediates: the
+//     offset of the operand byte), bit 30 page-cross penalty, bit 31 RAM
+//   C_STTIA: TIA register << 8 (the log entry's register field); C_TLD/C_TBIT: address bit 0
+//   C_TR: destination register; C_JMP: target
+//   C_BR: [0:12) low bits of the taken target (same window), [16:24) flag mask
+constexpr uint32_t OPND = 16;
+constexpr uint32_t PEN = 1u << 30, RAM = 1u << 31;
 }  // namespace pd
 
 // fast-path classes; 0 = general interpreter
@@ -49,13 +52,13 @@ enum PClass : uint32_t {
   C_WSYNC,  // store to WSYNC (direct)
   C_INC, C_DEC, C_ASL, C_LSR, C_ROL, C_ROR,  // read-modify-write of RAM
   C_INR,    // INX/INY/DEX/DEY, AUX as K_INR
-  C_TR,     // transfers, AUX bits 0-1 source, bit 2 (set N,Z) — destination in REG field
+  C_TR,     // transfers, AUX bits 0-1 source, bit 2 (set N,Z); destination in hi
   C_FLAG,   // flag set/clear, AUX as K_FLAG
   C_ASLA, C_LSRA, C_ROLA, C_RORA,
   C_NOP,    // implied NOP
-  C_BR,     // conditional branch: AUX bits 0-1 source (0 nreg, 1 V, 2 C, 3 zreg), REG mask, AUX
-            // bit 2 = taken when (source & mask) != 0
-  C_JMP,    // JMP absolute
+  C_BR,     // conditional branch inside the window: AUX bits 0-1 source (0 nreg, 1 V, 2 C,
+            // 3 zreg), bit 2 = taken when (source & mask) != 0
+  C_JMP,    // JMP absolute into cartridge space
   C_COUNT
 };
 static_assert(C_COUNT <= 32, "class field is 5 bits");
@@ -68,12 +71,13 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
   const uint64_t ent = stab[op];
   const uint32_t d = (uint32_t)ent, e = (uint32_t)(ent >> 32);
   const uint32_t kind = e & 0xFFu, aux = (e >> sk::AUX) & 0x7Fu;
-  const uint32_t len = (d >> sk::LEN) & 3u, cyc = (d >> sk::CYC) & 0xFu;
+  const uint32_t len = (d >> sk::LEN) & 3u;
+  uint32_t cyc = (d >> sk::CYC) & 0xFu;
   const uint32_t sel = d & 0xFFFFu;
   const uint32_t b1 = o + 1 <= 0xFFFu ? bank[o + 1] : 0u, b2 = o + 2 <= 0xFFFu ? bank[o + 2] : 0u;
   const uint32_t base = b1 | (b2 << 8);
-  uint32_t cls = C_GEN, opnd = 0, raux = 0, reg = 0;
-  bool ram = false, pen = (d & sk::PEN) != 0u;
+  uint32_t cls = C_GEN, raux = 0;
+  const bool pen = (d & sk::PEN) != 0u;
   // the whole instruction must be fetched from this bank window without touching a hotspot
   bool fast = kind != K_JAM && o + len - 1 <= 0xFFFu;
   if (f8)
@@ -108,7 +112,14 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
     if (f8 && lo + 255u >= 0xFF8u) return 0;
     return 2;
   };
+  // the fall-through PC must stay inside the window (its low 12 bits are stored)
+  if (o + len > 0xFFFu) fast = false;
+  uint32_t hi = 0;
   if (fast) {
+    auto mem = [&](uint32_t cl, uint32_t off, bool is_ram) {
+      cls = cl;
+      hi = sel | ((off & 0xFFFu) << pd::OPND) | (pen ? pd::PEN : 0u) | (is_ram ? pd::RAM : 0u);
+    };
     switch (kind) {
       case K_ORA: case K_AND: case K_EOR: case K_ADC: case K_SBC: case K_CMP: case K_BIT: case K_LD:
       case K_NOP: {
@@ -117,58 +128,57 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
                               kind == K_ADC ? C_ADC : kind == K_SBC ? C_SBC : kind == K_CMP ? C_CMP :
                               kind == K_BIT ? C_BIT : kind == K_LD ? C_LD : C_NOPR;
         raux = aux & 7u;
-        if (imm) { cls = rcls; opnd = o + 1; break; }
+        if (imm) { mem(rcls, o + 1, false); break; }
         const int w = where();
-        if (w == 1) { cls = rcls; ram = true; opnd = zp ? b1 : (base & 0x7Fu) | 0x80u; }  // = base if indexed
-        else if (w == 2) { cls = rcls; opnd = base & 0xFFFu; }
-        else if (w == 4 && kind == K_LD) { cls = C_TLD; opnd = base & 0x1FFFu; }
-        else if (w == 4 && kind == K_BIT) { cls = C_TBIT; opnd = base & 0x1FFFu; }
+        if (w == 1) mem(rcls, zp ? b1 : (base & 0x7Fu) | 0x80u, true);  // = base if indexed
+        else if (w == 2) mem(rcls, base, false);
+        else if (w == 4 && kind == K_LD) { cls = C_TLD; hi = base & 1u; }
+        else if (w == 4 && kind == K_BIT) { cls = C_TBIT; hi = base & 1u; }
         break;
       }
       case K_ST: {
         const int w = where();
         raux = aux & 3u;
-        if (w == 1) { cls = C_STRAM; ram = true; opnd = zp ? b1 : (base & 0x7Fu) | 0x80u; }
+        if (w == 1) mem(C_STRAM, zp ? b1 : (base & 0x7Fu) | 0x80u, true);
         else if (w == 3 && !indexed) {
           const uint32_t r = (zp ? b1 : base) & 0x3Fu;
           // TIA writes with a picture effect: 0x01, 0x04-0x14, 0x1B-0x2C (scalar_cpu.cuh kTiaEffect)
           const bool eff = r == 0x01u || (r >= 0x04u && r <= 0x14u) || (r >= 0x1Bu && r <= 0x2Cu);
-          if (eff) { cls = C_STTIA; reg = r; }
+          if (eff) { cls = C_STTIA; hi = r << 8; }
           else if (r == 0x02u) cls = C_WSYNC;
         }
         break;
       }
       case K_INC: case K_DEC: case K_ASL: case K_LSR: case K_ROL: case K_ROR: {
-        if (where() == 1) {
-          cls = kind == K_INC ? C_INC : kind == K_DEC ? C_DEC : kind == K_ASL ? C_ASL :
-                kind == K_LSR ? C_LSR : kind == K_ROL ? C_ROL : C_ROR;
-          ram = true;
-          opnd = zp ? b1 : (base & 0x7Fu) | 0x80u;
-        }
+        if (where() == 1)
+          mem(kind == K_INC ? C_INC : kind == K_DEC ? C_DEC : kind == K_ASL ? C_ASL :
+              kind == K_LSR ? C_LSR : kind == K_ROL ? C_ROL : C_ROR, zp ? b1 : (base & 0x7Fu) | 0x80u, true);
         break;
       }
       case K_INR: cls = C_INR; raux = aux & 3u; break;
-      case K_TR: cls = C_TR; raux = (aux & 3u) | ((aux & 16u) ? 4u : 0u); reg = (aux >> 2) & 3u; break;
+      case K_TR: cls = C_TR; raux = (aux & 3u) | ((aux & 16u) ? 4u : 0u); hi = (aux >> 2) & 3u; break;
       case K_FLAG: cls = C_FLAG; raux = aux & 7u; break;
       case K_ASLA: cls = C_ASLA; break;
       case K_LSRA: cls = C_LSRA; break;
       case K_ROLA: cls = C_ROLA; break;
       case K_RORA: cls = C_RORA; break;
-      case K_BR: {  // taken iff ((flag source & REG mask) != 0) == AUX bit 2 (see C_BR)
+      case K_BR: {  // taken iff ((flag source & mask) != 0) == AUX bit 2 (see C_BR)
+        const int32_t from = (int32_t)o + 2, tgt = from + (int32_t)(int8_t)b1;
+        if (tgt < 0 || tgt > 0xFFF) break;  // the target leaves the window: general path
         const uint32_t f = aux & 3u, want = (aux >> 2) & 1u;
+        const uint32_t mask = f == 0u ? 0x80u : (f == 3u ? 0xFFu : 0x01u);  // N: bit 7 of nreg; Z: zreg & 0xFF
         cls = C_BR;
-        reg = f == 0u ? 0x80u : (f == 3u ? 0xFFu : 0x01u);  // N: bit 7 of nreg; Z: zreg & 0xFF
         raux = f | ((want ^ (f == 3u ? 1u : 0u)) << 2);
-        opnd = b1;
+        cyc = 3u + ((((uint32_t)from ^ (uint32_t)tgt) >> 8) & 1u);
+        hi = (uint32_t)tgt | (mask << 16);
       } break;
-      case K_JMP: if (!ptr) { cls = C_JMP; opnd = base; } break;
+      case K_JMP:
+        if (!ptr && (base & 0x1000u)) { cls = C_JMP; hi = base; }  // the target is cartridge space
+        break;
       default: break;
     }
   }
-  uint32_t lo = op | (cls << pd::CLS) | (len << pd::LEN) | (cyc << pd::CYC) | (raux << pd::AUX) | (reg << pd::REG);
-  if (pen) lo |= pd::PEN;
-  if (ram) lo |= pd::RAM;
-  const uint32_t hi = (opnd & 0xFFFFu) | (sel << 16);
+  const uint32_t lo = cls | (raux << pd::AUX) | (cyc << pd::CYC) | (((o + len) & 0xFFFu) << pd::NXT);
   return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
