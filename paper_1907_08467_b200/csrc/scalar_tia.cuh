@@ -342,6 +342,7 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
     const uint32_t e = lg[k];
     const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
     catch_up_coop(t, T, rb, lane, ystart, gray, w, dirty);
+    __syncwarp();  // reconverge: the register update is warp-uniform work, issued once
     t.apply(r, e & 0xFFu, T);
     dirty |= kDirtyTable.v[r];
   }
