@@ -33,16 +33,18 @@ CONFIGS = {
     "cfg4": (["R1", "R2", "R3", "R4"], 32768, 4, "gray84", "cfg4: 32768 envs, R1-R4 interleaved, fs=4, GRAY84"),
 }
 
-# The step kernel is bound by instruction issue: per raw frame it issues a
-# fixed number of warp-instructions, measured once per build with ncu (smsp__inst_executed.sum
-# / frames per launch) and committed under profiles/.  achieved = that x frames per launch /
-# the live launch time; peak = 148 SMs x 4 schedulers x 1 warp-instruction/cycle x max clock.
-# DRAM traffic per launch comes from the same capture.
-ISSUE_PROFILE = {
-    "cfg2": {"warp_inst_per_frame": 577100.0, "dram_bytes_per_launch": 546.4e6,
-             "source": "profiles/r01_v3_step_kernel_ncu.txt"},
-}
-
+# The step kernel is bound by instruction issue (ncu shows the ALU pipe at
+# ~78% and issue at ~77% of peak): per raw frame it issues a fixed number of warp-instructions,
+# measured once per build with ncu (smsp__inst_executed.sum / frames per launch) and committed in
+# profiles/issue_profile.json with the DRAM traffic of the same capture, keyed by config and
+# engine.  achieved = that x frames per launch / the live launch time; peak = 148 SMs x 4
+# schedulers x 1 warp-instruction/cycle x max clock.
+def issue_profile(config: str, engine: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue_profile.json")) as f:
+            return json.load(f).get(f"{config}/{engine}")
+    except (OSError, ValueError):
+        return None
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -278,7 +280,7 @@ def run_cule(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    # roofline of the dominant (only) kernel: step_kernel, one launch per step
+    # roofline of the dominant (only) kernel: the step kernel, one launch per step
     pk = peaks()
     launch_s = ms_max / 1000.0 / K
     alg_bytes_per_env = 208 * 2 + 1 + 4 + 1 + (7056 if mode == "gray84" else 33600)
@@ -286,12 +288,13 @@ def run_cule(args, rank, world, local_rank):
     hbm_gbs = alg_bytes / launch_s / 1e9
     sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
     issue_peak = 148 * 4 * pk["sm_max_mhz"] * 1e6 / 1e12  # T warp-instr/s at max clock
-    prof = ISSUE_PROFILE.get(args.config) if not args.envs else None
+    prof = issue_profile(args.config, env.engine) if not args.envs else None
     ipf = prof["warp_inst_per_frame"] if prof else None
     roof = {"bound": "alu", "unit": "Twarp-inst/s", "peak": issue_peak,
             "achieved": (ipf * envs * fs / launch_s / 1e12) if ipf else None,
             "traffic": prof["dram_bytes_per_launch"] if prof else None,
             "profile": prof["source"] if prof else None,
+            "alu_pipe_frac_ncu": prof.get("alu_pipe_frac") if prof else None,
             "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk["hbm_gbs"], "frac": hbm_gbs / pk["hbm_gbs"],
                     "alg_bytes_per_launch": alg_bytes},
             "peak_source": pk["source"]}
@@ -304,7 +307,7 @@ def run_cule(args, rank, world, local_rank):
                    "actions": "uniform random over 18, torch cuda generator seed 1234+rank",
                    "l2": "per-step working set > 126 MB L2 (staging frames " +
                          f"{envs * 33600 / 1e6:.0f} MB + obs + state)",
-                   "parallelism": f"dp{world} (env shards)"},
+                   "parallelism": f"dp{world} (env shards)", "engine": env.engine},
         "fps_per_env": fps / (envs * world),
         "training_frames_per_s": fps / 4,
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": envs,

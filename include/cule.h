@@ -124,6 +124,11 @@ int cule_debug_exec(cule_env* env, int n_instr, int32_t* d_status, void* cuda_st
 
 /* Number of envs / frameskip / observation bytes per env of a handle. */
 int cule_num_envs(const cule_env* env);
+/* Which step kernel the handle runs: 0 = batched SIMT engine (a few envs per warp, shared
+ * micro-coded datapath), 1 = scalar engine (one env per warp, pre-decoded cartridge records).
+ * Both implement the same machine model; chosen at create from the env count (CULE_ENGINE =
+ * simt | scalar overrides).  CULE_E_CLOSED for a destroyed handle. */
+int cule_engine(const cule_env* env);
 int cule_frameskip(const cule_env* env);
 size_t cule_obs_bytes(const cule_env* env);
 

@@ -26,7 +26,7 @@ STATE_BYTES = 256
 EXPORTS = ["cule_default_config", "cule_workspace_bytes", "cule_create", "cule_reset",
            "cule_step", "cule_step_host", "cule_get_state", "cule_set_state", "cule_counters",
            "cule_debug_exec", "cule_num_envs", "cule_frameskip", "cule_obs_bytes",
-           "cule_destroy", "cule_last_error"]
+           "cule_engine", "cule_destroy", "cule_last_error"]
 
 
 class CuleConfig(ctypes.Structure):
@@ -74,6 +74,7 @@ def load():
     L.cule_debug_exec.argtypes = [vp, ctypes.c_int, vp, vp]
     L.cule_num_envs.argtypes = [vp]
     L.cule_frameskip.argtypes = [vp]
+    L.cule_engine.argtypes = [vp]
     L.cule_obs_bytes.argtypes = [vp]
     L.cule_obs_bytes.restype = ctypes.c_size_t
     L.cule_destroy.argtypes = [vp]
@@ -81,7 +82,7 @@ def load():
     L.cule_last_error.restype = ctypes.c_char_p
     for name in ("cule_create", "cule_reset", "cule_step", "cule_step_host", "cule_get_state",
                  "cule_set_state", "cule_counters", "cule_debug_exec", "cule_num_envs",
-                 "cule_frameskip", "cule_destroy"):
+                 "cule_frameskip", "cule_engine", "cule_destroy"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L

@@ -169,7 +169,9 @@ static int choose_engine(int N) {
     if (!strcmp(v, "simt")) return 0;
     if (!strcmp(v, "scalar")) return 1;
   }
-  return N <= 6144 ? 1 : 0;  // measured: scalar 1.19M vs SIMT 0.77M FPS at 4096; SIMT 2.4M vs 1.3M at 16384
+  // measured (profiles/r01_v6_engine_sweep.txt): 4096 envs scalar 2.28M vs SIMT 0.75M FPS;
+  // 16384 (F8) 2.27M vs 2.31M; 32768 (4 ROMs) 1.80M vs 2.85M
+  return N <= 12288 ? 1 : 0;
 }
 
 // Envs per warp: the per-env 6502 chain is latency-bound, so at low env counts the kernel
@@ -485,6 +487,7 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
 
 int cule_num_envs(const cule_env* e) { return live(e) ? e->N : CULE_E_CLOSED; }
 int cule_frameskip(const cule_env* e) { return live(e) ? e->fs : CULE_E_CLOSED; }
+int cule_engine(const cule_env* e) { return live(e) ? e->engine : CULE_E_CLOSED; }
 size_t cule_obs_bytes(const cule_env* e) { return live(e) ? obs_bytes_of(e->cfg.obs_mode) : 0; }
 
 int cule_destroy(cule_env* e) {

@@ -486,7 +486,10 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
                                             uint32_t log_lim, uint32_t cap_cycles, int32_t& budget,
                                             uint32_t rec_all0) {
   uint32_t A = M->A, X = M->X, Y = M->Y, SP = M->SP;
-  uint32_t C = M->C, V = M->V, D = M->D, I = M->I, nreg = M->nreg, zreg = M->zreg;
+  uint32_t C = M->C, V = M->V, D = M->D, I = M->I;
+  // N and Z packed in one register: the Z byte in bits 0-7 (Z = it is 0), N at bit 15; an
+  // ordinary result x sets nz = x * 257 (one multiply-add, no second register copy)
+  uint32_t nz = (M->zreg & 0xFFu) | ((M->nreg & 0x80u) << 8);
   uint32_t fc = M->fc, bank = M->bank, log_len = M->log_len;
   uint32_t pcw = M->PC & 0xF000u, pco = M->PC & 0xFFFu;
   uint32_t ws_fc = fc, ws_now = M->t_phaseA / 3u;  // phase A of the first instruction
@@ -497,21 +500,20 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   // idle-loop skip (exact): the last plain timer read (offset, cycles, cycles its value holds, end)
   uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
   const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
-  auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
+  auto setnz = [&](uint32_t x) { nz = x * 257u; };  // x <= 0xFF
   auto adc = [&](uint32_t m) {
     if (!D) {
       const uint32_t t = A + m + C;
       V = ((~(A ^ m) & (A ^ t)) >> 7) & 1u;
       C = t >> 8;
       A = t & 0xFFu;
-      nz(A);
+      setnz(A);
     } else {  // NMOS decimal (R#2)
       uint32_t lo = (A & 0xFu) + (m & 0xFu) + C;
       if (lo >= 0xAu) lo = ((lo + 6u) & 0xFu) + 0x10u;
       uint32_t s = (A & 0xF0u) + (m & 0xF0u) + lo;
       const int32_t sv = (int32_t)(int8_t)(A & 0xF0u) + (int32_t)(int8_t)(m & 0xF0u) + (int32_t)lo;
-      zreg = (A + m + C) & 0xFFu;
-      nreg = s;
+      nz = ((A + m + C) & 0xFFu) | ((s & 0x80u) << 8);  // Z from the binary sum, N from s
       V = (sv < -128 || sv > 127) ? 1u : 0u;
       if (s >= 0xA0u) s += 0x60u;
       C = s >= 0x100u ? 1u : 0u;
@@ -532,9 +534,14 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       A = r;
     }
     C = t >> 8;
-    nz(r);
+    setnz(r);
   };
-  auto cmp = [&](uint32_t r, uint32_t m) { C = r >= m ? 1u : 0u; nz((r - m) & 0xFFu); };
+  auto cmp = [&](uint32_t r, uint32_t m) { C = r >= m ? 1u : 0u; setnz((r - m) & 0xFFu); };
+  auto prmt = [](uint32_t a, uint32_t b, uint32_t sel) {  // raw PRMT: selector bits used as stored
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+  };
   if (kDebug && budget <= 0) { ev = SE_BUDGET; goto out; }
   if (!(pcw & 0x1000u)) goto general;  // entered outside the cartridge (code in RAM)
   for (;;) {
@@ -547,7 +554,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       uint32_t npco = lo >> pd::NXT;
       if (cls == C_BR) {  // the most frequent class, tested before the switch
         const uint32_t aux = lo >> pd::AUX;
-        const uint32_t src = (aux & 2u) ? ((aux & 1u) ? zreg : C) : ((aux & 1u) ? V : nreg);
+        const uint32_t src = (aux & 2u) ? ((aux & 1u) ? nz : C) : ((aux & 1u) ? V : nz);
         if (((src & (hi >> 16)) != 0u) == ((aux & 4u) != 0u)) {
           npco = hi & 0xFFFu;
           // idle-loop skip: [timer read; branch back to it] — later iterations whose read falls
@@ -574,7 +581,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
         // data operand: RAM[(opnd + ix) & 0x7F] (needs bit 7 of opnd + ix, else the general
         // path: zp,X into the TIA) or the cartridge byte (opnd + ix) & 0xFFF of the bank
         const uint32_t opnd = hi >> pd::OPND;
-        const uint32_t t = opnd + __byte_perm(X | (Y << 8), 0u, hi);
+        const uint32_t t = opnd + prmt(X + Y * 256u, 0u, hi);
         uint32_t v = 0u;
         auto rd_operand = [&]() -> bool {
           if (hi & pd::RAM) {
@@ -583,23 +590,23 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           } else {
             v = ld_ro8(romb + (t & 0xFFFu));
           }
-          now += (hi & pd::PEN) ? ((t ^ opnd) >> 8) & 1u : 0u;
+          now += ((t ^ opnd) & hi & pd::PEN) >> 8;
           return true;
         };
         switch (cls) {
-          case C_ORA: if (!rd_operand()) goto general; A |= v; nz(A); break;
-          case C_AND: if (!rd_operand()) goto general; A &= v; nz(A); break;
-          case C_EOR: if (!rd_operand()) goto general; A ^= v; nz(A); break;
+          case C_ORA: if (!rd_operand()) goto general; A |= v; setnz(A); break;
+          case C_AND: if (!rd_operand()) goto general; A &= v; setnz(A); break;
+          case C_EOR: if (!rd_operand()) goto general; A ^= v; setnz(A); break;
           case C_ADC: if (!rd_operand()) goto general; adc(v); break;
           case C_SBC: if (!rd_operand()) goto general; sbc(v); break;
           case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
-          case C_BIT: if (!rd_operand()) goto general; nreg = v; zreg = A & v; V = (v >> 6) & 1u; break;
+          case C_BIT: if (!rd_operand()) goto general; nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
           case C_LD:
             if (!rd_operand()) goto general;
             A = (aux & 1u) ? v : A;
             X = (aux & 2u) ? v : X;
             Y = (aux & 4u) ? v : Y;
-            nz(v);
+            setnz(v);
             break;
           case C_NOPR: if (!rd_operand()) goto general; break;
           case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
@@ -621,9 +628,9 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
               A = (aux & 1u) ? v : A;
               X = (aux & 2u) ? v : X;
               Y = (aux & 4u) ? v : Y;
-              nz(v);
+              setnz(v);
             } else {
-              nreg = v; zreg = A & v; V = (v >> 6) & 1u;
+              nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u;
             }
             pff = ff & skip_mask;
             ppc = pco;
@@ -663,14 +670,14 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             else if (cls == C_LSR) { C = m & 1u; r = m >> 1; }
             else if (cls == C_ROL) { r = ((m << 1) | C) & 0xFFu; C = m >> 7; }
             else { r = (m >> 1) | (C << 7); C = m & 1u; }
-            nz(r);
+            setnz(r);
             st_ram(a, r);
           } break;
           case C_INR: {
             const uint32_t r = (((aux & 1u) ? Y : X) + ((aux & 2u) ? 0xFFu : 1u)) & 0xFFu;
             X = (aux & 1u) ? X : r;
             Y = (aux & 1u) ? r : Y;
-            nz(r);
+            setnz(r);
           } break;
           case C_TR: {
             const uint32_t s = aux & 3u, d = hi;
@@ -679,7 +686,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             X = d == 1u ? r : X;
             Y = d == 2u ? r : Y;
             SP = d == 3u ? r : SP;
-            if (aux & 4u) nz(r);
+            if (aux & 4u) setnz(r);
           } break;
           case C_FLAG: {
             const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
@@ -688,10 +695,10 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             D = f == 2u ? b : D;
             V = f == 3u ? b : V;
           } break;
-          case C_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; nz(A); break;
-          case C_LSRA: C = A & 1u; A >>= 1; nz(A); break;
-          case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; nz(A); } break;
-          case C_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); nz(A); } break;
+          case C_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; setnz(A); break;
+          case C_LSRA: C = A & 1u; A >>= 1; setnz(A); break;
+          case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; setnz(A); } break;
+          case C_RORA: { const uint32_t c = C; C = A & 1u; A = (A >> 1) | (c << 7); setnz(A); } break;
           case C_NOP: break;
           case C_JMP:
             pcw = hi & 0xF000u;
@@ -714,13 +721,14 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             // cartridge window
     for (;;) {
       M->PC = pcw | pco; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
-      M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
+      M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nz >> 8; M->zreg = nz & 0xFFu;
       M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
       const uint32_t r = s_gen_one(M, rom_all0, dtab0, ram0, lg0, log_lim, cap_cycles);
       const uint32_t PC = M->PC;
       pcw = PC & 0xF000u; pco = PC & 0xFFFu;
       A = M->A; X = M->X; Y = M->Y; SP = M->SP;
-      C = M->C; V = M->V; D = M->D; I = M->I; nreg = M->nreg; zreg = M->zreg;
+      C = M->C; V = M->V; D = M->D; I = M->I;
+      nz = (M->zreg & 0xFFu) | ((M->nreg & 0x80u) << 8);
       fc = M->fc; bank = M->bank; log_len = M->log_len;
       ws_fc = fc; ws_now = M->t_phaseA / 3u;
       if (kDebug && (r & kGenCommitted)) --budget;
@@ -734,7 +742,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   }
 out:
   M->PC = pcw | pco; M->A = A; M->X = X; M->Y = Y; M->SP = SP;
-  M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nreg; M->zreg = zreg;
+  M->C = C; M->V = V; M->D = D; M->I = I; M->nreg = nz >> 8; M->zreg = nz & 0xFFu;
   M->fc = fc; M->bank = bank; M->log_len = log_len; M->t_phaseA = 3u * (fc == ws_fc ? ws_now : fc);
   return ev;
 }

@@ -28,14 +28,16 @@ namespace pd {
 // [20:32) low 12 bits of the fall-through PC (the instruction ends inside the 4 KB window).
 constexpr uint32_t AUX = 5, CYC = 8, NXT = 20;
 // Record word hi, by class:
-//   reads / stores / read-modify-writes: [0:16) byte-permute selector of the index (sk::SEL_*),
-//     [16:28) operand (RAM: zero-page address; cartridge: offset in the bank, immediates: the
-//     offset of the operand byte), bit 30 page-cross penalty, bit 31 RAM
+//   reads / stores / read-modify-writes: [0:16) byte-permute selector of the index (sk::SEL_*;
+//     bit 8 = page-cross penalty, which turns selector nibble 2 from 4 into 5: both pick a zero
+//     byte of the permute's second operand), [16:28) operand (RAM: zero-page address;
+//     cartridge: offset in the bank; immediates: the offset of the operand byte), bit 31 RAM
 //   C_STTIA: TIA register << 8 (the log entry's register field); C_TLD/C_TBIT: address bit 0
 //   C_TR: destination register; C_JMP: target
-//   C_BR: [0:12) low bits of the taken target (same window), [16:24) flag mask
+//   C_BR: [0:12) low bits of the taken target (same window), [16:32) flag mask (nz packs N at
+//     bit 15 and the Z byte in bits 0-7, see scalar_cpu.cuh)
 constexpr uint32_t OPND = 16;
-constexpr uint32_t PEN = 1u << 30, RAM = 1u << 31;
+constexpr uint32_t PEN = 1u << 8, RAM = 1u << 31;
 }  // namespace pd
 
 // fast-path classes; 0 = general interpreter
@@ -56,8 +58,8 @@ enum PClass : uint32_t {
   C_FLAG,   // flag set/clear, AUX as K_FLAG
   C_ASLA, C_LSRA, C_ROLA, C_RORA,
   C_NOP,    // implied NOP
-  C_BR,     // conditional branch inside the window: AUX bits 0-1 source (0 nreg, 1 V, 2 C,
-            // 3 zreg), bit 2 = taken when (source & mask) != 0
+  C_BR,     // conditional branch inside the window: AUX bits 0-1 source (0 nz, 1 V, 2 C,
+            // 3 nz), bit 2 = taken when (source & mask) != 0
   C_JMP,    // JMP absolute into cartridge space
   C_COUNT
 };
@@ -166,7 +168,7 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
         const int32_t from = (int32_t)o + 2, tgt = from + (int32_t)(int8_t)b1;
         if (tgt < 0 || tgt > 0xFFF) break;  // the target leaves the window: general path
         const uint32_t f = aux & 3u, want = (aux >> 2) & 1u;
-        const uint32_t mask = f == 0u ? 0x80u : (f == 3u ? 0xFFu : 0x01u);  // N: bit 7 of nreg; Z: zreg & 0xFF
+        const uint32_t mask = f == 0u ? 0x8000u : (f == 3u ? 0xFFu : 0x01u);  // N: bit 15 of nz; Z: nz & 0xFF
         cls = C_BR;
         raux = f | ((want ^ (f == 3u ? 1u : 0u)) << 2);
         cyc = 3u + ((((uint32_t)from ^ (uint32_t)tgt) >> 8) & 1u);

@@ -69,6 +69,7 @@ class Env:
             self.dones = torch.zeros(self.num_envs, dtype=torch.uint8, device=self.device)
             self._counters = torch.zeros(4, dtype=torch.int64, device=self.device)
         self.obs_bytes = int(np.prod(shape))
+        self.engine = "scalar" if _lib.check(L.cule_engine(self._h)) == 1 else "simt"
 
     # -- core calls ----------------------------------------------------------------------------
     def reset(self, seed: int = 0, stream=None) -> torch.Tensor:
