@@ -593,14 +593,10 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           now += ((t ^ opnd) & hi & pd::PEN) >> 8;
           return true;
         };
-        switch (cls) {
-          case C_ORA: if (!rd_operand()) goto general; A |= v; setnz(A); break;
-          case C_AND: if (!rd_operand()) goto general; A &= v; setnz(A); break;
-          case C_EOR: if (!rd_operand()) goto general; A ^= v; setnz(A); break;
-          case C_ADC: if (!rd_operand()) goto general; adc(v); break;
+        if (cls <= C_HOT_LAST) {
+          switch (cls) {
           case C_SBC: if (!rd_operand()) goto general; sbc(v); break;
           case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
-          case C_BIT: if (!rd_operand()) goto general; nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
           case C_LD:
             if (!rd_operand()) goto general;
             A = (aux & 1u) ? v : A;
@@ -608,7 +604,6 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             Y = (aux & 4u) ? v : Y;
             setnz(v);
             break;
-          case C_NOPR: if (!rd_operand()) goto general; break;
           case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
             const int32_t et = (int32_t)now - M->tW;
             const uint32_t tV = M->tV, tS = M->tS;
@@ -637,10 +632,6 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             pn = now - fc;
             pfe = now;
           } break;
-          case C_STRAM:
-            if (!(t & 0x80u)) goto general;
-            st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
-            break;
           case C_STTIA: {
             const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
             st_log(lg0 + 4u * log_len, ((3u * now) << 14) | hi | wv);
@@ -658,6 +649,36 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             ws_now = now;
             now = ((now + 75u) / 76u) * 76u;
             ws_fc = now;
+            break;
+          case C_TR: {
+            const uint32_t s = aux & 3u, d = hi;
+            const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
+            A = d == 0u ? r : A;
+            X = d == 1u ? r : X;
+            Y = d == 2u ? r : Y;
+            SP = d == 3u ? r : SP;
+            if (aux & 4u) setnz(r);
+          } break;
+          case C_FLAG: {
+            const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
+            C = f == 0u ? b : C;
+            I = f == 1u ? b : I;
+            D = f == 2u ? b : D;
+            V = f == 3u ? b : V;
+          } break;
+          default: goto general;
+          }
+        } else {
+          switch (cls) {
+          case C_ORA: if (!rd_operand()) goto general; A |= v; setnz(A); break;
+          case C_AND: if (!rd_operand()) goto general; A &= v; setnz(A); break;
+          case C_EOR: if (!rd_operand()) goto general; A ^= v; setnz(A); break;
+          case C_ADC: if (!rd_operand()) goto general; adc(v); break;
+          case C_BIT: if (!rd_operand()) goto general; nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
+          case C_NOPR: if (!rd_operand()) goto general; break;
+          case C_STRAM:
+            if (!(t & 0x80u)) goto general;
+            st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
             break;
           case C_INC: case C_DEC: case C_ASL: case C_LSR: case C_ROL: case C_ROR: {
             if (!(t & 0x80u)) goto general;
@@ -679,22 +700,6 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             Y = (aux & 1u) ? r : Y;
             setnz(r);
           } break;
-          case C_TR: {
-            const uint32_t s = aux & 3u, d = hi;
-            const uint32_t r = s == 0u ? A : (s == 1u ? X : (s == 2u ? Y : SP));
-            A = d == 0u ? r : A;
-            X = d == 1u ? r : X;
-            Y = d == 2u ? r : Y;
-            SP = d == 3u ? r : SP;
-            if (aux & 4u) setnz(r);
-          } break;
-          case C_FLAG: {
-            const uint32_t f = aux & 3u, b = (aux >> 2) & 1u;
-            C = f == 0u ? b : C;
-            I = f == 1u ? b : I;
-            D = f == 2u ? b : D;
-            V = f == 3u ? b : V;
-          } break;
           case C_ASLA: C = A >> 7; A = (A << 1) & 0xFFu; setnz(A); break;
           case C_LSRA: C = A & 1u; A >>= 1; setnz(A); break;
           case C_ROLA: { const uint32_t c = C; C = A >> 7; A = ((A << 1) | c) & 0xFFu; setnz(A); } break;
@@ -706,6 +711,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             if (!kDebug && now >= cap_cycles) { pco = npco; fc = now; M->fault = 2u; ev = SE_FAULT; goto out; }
             break;
           default: goto general;
+          }
         }
       }
     fast_done:

@@ -46,24 +46,26 @@ enum PClass : uint32_t {
   // reads: v = RAM[(opnd + ix) & 0x7F] (RAM; needs bit 7 of opnd + ix, else GEN) or the
   // cartridge byte at offset (opnd + ix) & 0xFFF of the current bank (immediates: opnd = the
   // offset of the operand byte); AUX = register (C_CMP: 0 A 1 X 2 Y, C_LD: bit mask 1 A 2 X 4 Y)
-  C_ORA, C_AND, C_EOR, C_ADC, C_SBC, C_CMP, C_BIT, C_LD, C_NOPR,
-  C_TLD,    // LDA/LDX/LDY/LAX of INTIM/TIMINT (absolute, RIOT timer closed form)
-  C_TBIT,   // BIT of INTIM/TIMINT (absolute)
+  // -- the classes most frequent after C_BR come first (1..C_HOT_LAST): the kernel dispatches
+  //    them through a separate, smaller switch
+  C_LD, C_STTIA, C_TLD, C_TBIT, C_TR, C_CMP, C_FLAG, C_SBC, C_WSYNC,
+  C_ORA, C_AND, C_EOR, C_ADC, C_BIT, C_NOPR,
   C_STRAM,  // store to RAM (zero page, zp indexed, or absolute RAM); AUX 0 A 1 X 2 Y 3 A&X
-  C_STTIA,  // store to a TIA register with a picture effect (direct): log append
-  C_WSYNC,  // store to WSYNC (direct)
   C_INC, C_DEC, C_ASL, C_LSR, C_ROL, C_ROR,  // read-modify-write of RAM
   C_INR,    // INX/INY/DEX/DEY, AUX as K_INR
-  C_TR,     // transfers, AUX bits 0-1 source, bit 2 (set N,Z); destination in hi
-  C_FLAG,   // flag set/clear, AUX as K_FLAG
   C_ASLA, C_LSRA, C_ROLA, C_RORA,
   C_NOP,    // implied NOP
   C_BR,     // conditional branch inside the window: AUX bits 0-1 source (0 nz, 1 V, 2 C,
             // 3 nz), bit 2 = taken when (source & mask) != 0
   C_JMP,    // JMP absolute into cartridge space
+  // C_TLD / C_TBIT: LDA/LDX/LDY/LAX / BIT of INTIM/TIMINT (absolute, RIOT timer closed form)
+  // C_STTIA: store to a TIA register with a picture effect (direct): log append
+  // C_WSYNC: store to WSYNC (direct); C_TR: transfers, AUX bits 0-1 source, bit 2 (set N,Z),
+  //   destination in hi; C_FLAG: flag set/clear, AUX as K_FLAG
   C_COUNT
 };
 static_assert(C_COUNT <= 32, "class field is 5 bits");
+constexpr uint32_t C_HOT_LAST = C_WSYNC;
 
 constexpr uint32_t kRecBytes = 8;
 

@@ -32,10 +32,19 @@ def _built():
     oracle.build()
 
 
+def check_engine(gpu):
+    """The engine the fixture asked for is the one that runs (the scalar engine needs its
+    pre-decoded records to fit in shared memory; a silent fallback would hide it from tests)."""
+    import os
+    want = os.environ.get("CULE_ENGINE")
+    assert gpu.engine == want, f"asked for the {want} engine, got {gpu.engine}"
+
+
 def pair(roms, n, fs, mode="gray84", **cfg):
     import oracle
     from paper_1907_08467_b200 import Env
     gpu = Env(roms, n, fs, obs_mode=mode, **cfg)
+    check_engine(gpu)
     ref = oracle.OracleEnv(roms, n, fs, H.palette_rgb(), obs_mode=1 if mode == "gray84" else 0, **cfg)
     return gpu, ref
 
@@ -195,18 +204,25 @@ def _random_states(n, n_roms, rng):
 
 
 @pytest.mark.parametrize("n_instr", [1, 3, 40])
-def test_random_instructions(n_instr):
+def test_random_instructions(n_instr, engine):
     """>= 1e5 random (opcode, registers, memory) cases through the debug entry of the kernel
-    against the oracle's single-instruction execution."""
+    against the oracle's single-instruction execution.  Random ROM bytes put
+    every opcode, addressing mode and operand at every offset, so the scalar engine's
+    pre-decoded fast classes and their edge cases (window-crossing branches, jumps into other
+    windows, zero-page indexing into the TIA, RAM-based abs,Y page crosses, F8 hotspots, code
+    in RAM) are all exercised.  Two 4 KB + one F8 ROM for the scalar engine (its records must fit
+    in shared memory), two of each for the batched engine."""
     import oracle
     from paper_1907_08467_b200 import Env
     rng = np.random.default_rng(100 + n_instr)
+    n_f8 = 1 if engine == "scalar" else 2
     roms = [rng.integers(0, 256, 4096, dtype=np.uint8).tobytes() for _ in range(2)] + \
-           [rng.integers(0, 256, 8192, dtype=np.uint8).tobytes() for _ in range(2)]
+           [rng.integers(0, 256, 8192, dtype=np.uint8).tobytes() for _ in range(n_f8)]
     n = 100_000 if n_instr == 1 else 20_000
     # RAW mode: no palette needed; only the debug entry is used (K=1 cache, 0 frames)
     gpu = Env(roms, n, 1, obs_mode="raw", reset_cache_size=1, startup_frames=0, max_random_frames=0)
-    st = _random_states(n, 4, rng)
+    check_engine(gpu)
+    st = _random_states(n, len(roms), rng)
     gpu.set_state(st)
     status = gpu.debug_exec(n_instr).cpu().numpy()
     got = gpu.get_state()
@@ -253,6 +269,8 @@ def test_num_envs_and_step_host_equivalence():
     big = Env([rom], 300, 4, reset_cache_size=6)
     small = Env([rom], 20, 4, reset_cache_size=6)
     host = Env([rom], 20, 4, reset_cache_size=6)
+    for e in (big, small, host):
+        check_engine(e)
     big.reset(9)
     small.reset(9)
     host.reset(9)
@@ -282,6 +300,7 @@ def test_sampled_parity_at_full_size(cfg):
     roms = [games.build_rom(n) for n in names]
     steps = 8
     gpu = Env(roms, N, 4)
+    check_engine(gpu)
     gpu.reset(0)
     acts = H.random_actions(N, steps, 99)
     rng = np.random.default_rng(1)
@@ -306,6 +325,7 @@ def test_sampled_parity_at_cfg2_size():
     rom = games.build_rom("R1")
     N, steps = 4096, 12
     gpu = Env([rom], N, 4)
+    check_engine(gpu)
     gpu.reset(0)
     acts = H.random_actions(N, steps, 1234)
     sample = np.unique(np.concatenate([np.arange(0, 16), np.arange(N - 8, N),
