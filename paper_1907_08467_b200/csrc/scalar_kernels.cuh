@@ -19,12 +19,16 @@
 namespace cule {
 
 // per-warp shared memory: [RAM 128][TIA words 48][SMach 128][state staging 80][log 4*kSLogCap]
+// [fused-observation ring 3 x 160]
 constexpr uint32_t kSLogCap = 128;
 constexpr uint32_t kSOffTia = 128, kSOffMach = 176, kSOffStg = 304, kSOffLog = 384;
-constexpr uint32_t kSWarpBytes = kSOffLog + 4 * kSLogCap;
+constexpr uint32_t kSOffRing = kSOffLog + 4 * kSLogCap;
+constexpr uint32_t kSWarpBytes = kSOffRing + 480;
 constexpr uint32_t kSWarps = CULE_SWARPS;  // warps per block (each warp emulates one env at a time)
 constexpr uint32_t kSmSDecode = kSmRom;  // scalar decode table [256] u64 right after the gray LUT
 constexpr uint32_t kSDecBytes = 2048;
+constexpr uint32_t kSmCols = kSmDecode;  // 84 packed area-average column weights (the batched
+                                         // engine's decode-table slot, unused by this kernel)
 
 // [header + gray][decode table][ROM images][records: 8 B per ROM byte, if staged][per-warp areas]
 __host__ __device__ __forceinline__ size_t scalar_rec_off(uint32_t rom_bytes) { return kSmSDecode + kSDecBytes + rom_bytes; }
@@ -132,13 +136,17 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
                                               uint32_t* lg, uint32_t* tw, uint32_t cap_cycles, uint32_t lane,
                                               uint32_t nframes, uint8_t* frame_out, uint32_t& episode_frames,
                                               int32_t budget, uint32_t ystart, const uint8_t* gray,
-                                              uint32_t rec_s) {
+                                              uint32_t rec_s, uint8_t* obs84, uint8_t* ring, const uint8_t* cols) {
   const uint32_t fill = kGray ? (uint32_t)gray[0] * 0x01010101u : 0u;
   RowBuf rb;
   rb.fill = fill;
   rb.render = false;
   rb.row = 0u;
   rb.frame = nullptr;
+  rb.obs84 = nullptr;
+  rb.prev = (kGray && nframes >= 2u) ? frame_out : nullptr;  // frame fs-1, staged by this step
+  rb.ring_s = smem_addr(ring);
+  rb.cols_s = smem_addr(cols);
   rb.r0 = rb.r1 = rb.r2 = rb.r3 = fill;
   uint32_t f = 0;
   int32_t status = RUN_FRAME;
@@ -147,7 +155,8 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
     rb.render = !kDebug && (kGray ? (f + 1 >= nframes) : (f == nframes));
     rb.row = 0u;
     rb.r0 = rb.r1 = rb.r2 = rb.r3 = fill;
-    rb.frame = (kGray && f == nframes) ? frame_out + kFrameBytes : frame_out;
+    rb.frame = frame_out;                               // GRAY84: frame fs-1; RAW: frame fs
+    rb.obs84 = (kGray && !kDebug && f == nframes) ? obs84 : nullptr;  // GRAY84 frame fs: fused
     ++episode_frames;
   };
   if (!kDebug && nframes == 0) return RUN_FRAME;
@@ -204,6 +213,8 @@ __device__ __forceinline__ void stage_block_s(const Params& p, uint8_t* smem) {
       if (p.use_rec) bulk_g2s(rec + kRecBytes * p.rom_off[r], p.srec + p.rom_off[r], kRecBytes * len, bar);
     }
   }
+  for (uint32_t j = threadIdx.x; j < 84u; j += blockDim.x)
+    reinterpret_cast<uint32_t*>(smem + kSmCols)[j] = area84_col(j);
   __syncthreads();
   mbar_wait(bar, 0);
 }
@@ -245,9 +256,11 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
   __syncwarp();
   uint8_t* frame_out = kDebug ? nullptr
                               : (kGray ? p.staging + (size_t)i * (2 * kFrameBytes) : p.obs + (size_t)i * kFrameBytes);
+  uint8_t* obs84 = (kGray && !kDebug) ? p.obs + (size_t)i * kObs84 : nullptr;
   const int32_t status = simulate_s<kGray, kDebug>(M, rom_all, dtab, ram, lg, tw, 76u * p.line_cap, lane,
                                                    kDebug ? 1u : p.fs, frame_out, episode_frames, p.debug_instr,
-                                                   p.ystart, gray, rec_s);
+                                                   p.ystart, gray, rec_s, obs84, wb + kSOffRing,
+                                                   smem + kSmCols);
   if (kDebug) {
     if (lane == 0u) {
       if (status == RUN_JAM) M->fault = 1u;
@@ -306,14 +319,10 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
     }
     st[lane * N + i] = v;
   }
-  // a5: observation
+  // a5: observation (GRAY84: already reduced row by row while frame fs was drawn; a faulted
+  // env's is zero)
   if (kGray) {
-    uint8_t* o = p.obs + (size_t)i * kObs84;
-    if (fault) warp_zero(o, kObs84, lane);
-    else {
-      const uint8_t* pair = p.staging + (size_t)i * (2 * kFrameBytes);
-      warp_area84(pair + kFrameBytes, p.fs >= 2 ? pair : nullptr, o, lane);
-    }
+    if (fault) warp_zero(p.obs + (size_t)i * kObs84, kObs84, lane);
   } else if (fault) {
     warp_zero(p.obs + (size_t)i * kFrameBytes, kFrameBytes, lane);
   }

@@ -214,9 +214,81 @@ struct RowBuf {
   uint32_t r0, r1, r2, r3;
   uint32_t row;       // warp-uniform: window row held (rows before it are stored)
   uint32_t fill;      // black, replicated (palette 0 or gray[0])
-  uint8_t* frame;     // 33,600-byte frame of this env
+  uint8_t* frame;     // 33,600-byte frame of this env (stored rows)
   bool render;
+  // fused observation (GRAY84, last frame of the step): completed rows are not stored; each is
+  // max-pooled with the same row of frame fs-1 (`prev`, staged in HBM; null for fs = 1) into a
+  // 3-row ring in shared memory, and every 2.5 rows an 84-pixel output row is reduced from it
+  uint8_t* obs84;     // u8[84][84] observation of this env, or null (store rows to `frame`)
+  const uint8_t* prev;
+  uint32_t ring_s;    // shared address of the 3 x 160-byte ring (per warp)
+  uint32_t cols_s;    // shared address of the 84 packed column weights (per block, area84_col)
 };
+
+// column weights of output column j (0..83) of the exact area average, packed c0 | wc0 << 8 |
+// wc1 << 16 | wc2 << 24: input columns c0..c0+2 with weights summing to 40 (40/21 per output
+// column; kernels.cuh warp_area84 computes the same inline)
+__device__ __forceinline__ uint32_t area84_col(uint32_t j) {
+  const uint32_t a = 40u * j, b = a + 40u;
+  const uint32_t c0 = a / 21u;
+  const uint32_t wc0 = min(b, 21u * (c0 + 1)) - a;
+  const uint32_t wc1 = min(b, 21u * (c0 + 2)) - 21u * (c0 + 1);
+  const uint32_t wc2 = b > 21u * (c0 + 2) ? b - 21u * (c0 + 2) : 0u;
+  return c0 | (wc0 << 8) | (wc1 << 16) | (wc2 << 24);
+}
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// output row i (0..83) of the exact area average from input rows r0, r0+1, r0+2 of the ring
+// (rows weighted 2:2:1 for even i, 1:2:2 for odd i; total weight 200, round half to even, R#17)
+__device__ __forceinline__ void area84_row(uint32_t ring_s, uint32_t cols_s, uint32_t r0, uint32_t i, uint8_t* out,
+                                           uint32_t lane) {
+  const uint32_t q0 = ring_s + (r0 % 3u) * 160u;
+  const uint32_t q1 = ring_s + ((r0 + 1u) % 3u) * 160u;
+  const uint32_t q2 = ring_s + ((r0 + 2u) % 3u) * 160u;
+  const uint32_t w0 = (i & 1u) ? 1u : 2u, w2 = (i & 1u) ? 2u : 1u;
+  uint8_t* orow = out + i * 84u;
+  for (uint32_t j = lane; j < 84u; j += 32u) {
+    uint32_t cw;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(cols_s + 4u * j) : "memory");
+    const uint32_t c0 = cw & 0xFFu, wc0 = (cw >> 8) & 0xFFu, wc1 = (cw >> 16) & 0xFFu, wc2 = cw >> 24;
+    const uint32_t c2 = wc2 ? c0 + 2u : c0;  // (weight 0: any in-row column)
+    const uint32_t s0 = wc0 * lds_u8(q0 + c0) + wc1 * lds_u8(q0 + c0 + 1u) + wc2 * lds_u8(q0 + c2);
+    const uint32_t s1 = wc0 * lds_u8(q1 + c0) + wc1 * lds_u8(q1 + c0 + 1u) + wc2 * lds_u8(q1 + c2);
+    const uint32_t s2 = wc0 * lds_u8(q2 + c0) + wc1 * lds_u8(q2 + c0 + 1u) + wc2 * lds_u8(q2 + c2);
+    const uint32_t S = w0 * s0 + 2u * s1 + w2 * s2;
+    uint32_t q = S / 200u;
+    const uint32_t r = S - 200u * q;
+    q += (r > 100u || (r == 100u && (q & 1u))) ? 1u : 0u;
+    orow[j] = (uint8_t)q;
+  }
+}
+
+// a completed row of the fused frame: max with frame fs-1 into the ring; rows 5k+2 and 5k+4
+// close output rows 2k and 2k+1 (rows 5k..5k+2 and 5k+2..5k+4)
+__device__ __forceinline__ void fused_row(const RowBuf& rb, uint32_t lane) {
+  const uint32_t r = rb.row;
+  const uint32_t slot = r % 3u;
+  if (lane < 10u) {
+    uint4 m = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
+    if (rb.prev) {
+      const uint4 q = reinterpret_cast<const uint4*>(rb.prev + r * 160u)[lane];
+      m.x = __vmaxu4(m.x, q.x); m.y = __vmaxu4(m.y, q.y); m.z = __vmaxu4(m.z, q.z); m.w = __vmaxu4(m.w, q.w);
+    }
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rb.ring_s + slot * 160u + 16u * lane), "r"(m.x),
+                 "r"(m.y), "r"(m.z), "r"(m.w) : "memory");
+  }
+  __syncwarp();
+  const uint32_t k = r % 5u;
+  if (k == 2u || k == 4u) {
+    area84_row(rb.ring_s, rb.cols_s, r - 2u, 2u * (r / 5u) + (k == 4u ? 1u : 0u), rb.obs84, lane);
+    __syncwarp();
+  }
+}
 
 // collision bits of visible pixels [xa, xb) reduced over the warp (even lanes 0..8 hold word lane/2)
 __device__ __forceinline__ uint32_t collide_coop(const Words& w, uint32_t lane, uint32_t xa, uint32_t xb) {
@@ -260,7 +332,8 @@ __device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t
 
 // store the completed row and start the next
 __device__ __forceinline__ void row_done(RowBuf& rb, uint32_t lane) {
-  if (lane < 10u) reinterpret_cast<uint4*>(rb.frame + rb.row * 160u)[lane] = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
+  if (rb.obs84) fused_row(rb, lane);
+  else if (lane < 10u) reinterpret_cast<uint4*>(rb.frame + rb.row * 160u)[lane] = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
   rb.r0 = rb.r1 = rb.r2 = rb.r3 = rb.fill;
   ++rb.row;
 }
@@ -356,7 +429,9 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
 // after the frame's last catch-up: store the partial row and black out the rows never reached
 __device__ __forceinline__ void finish_frame_coop(RowBuf& rb, uint32_t lane) {
   if (!rb.render) return;
-  if (rb.row < (uint32_t)kFrameH) {
+  if (rb.obs84) {  // the partial row, then black rows, through the fused reduction
+    while (rb.row < (uint32_t)kFrameH) row_done(rb, lane);
+  } else if (rb.row < (uint32_t)kFrameH) {
     if (lane < 10u) reinterpret_cast<uint4*>(rb.frame + rb.row * 160u)[lane] = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
     const uint32_t first = (rb.row + 1u) * 10u;
     uint4* p = reinterpret_cast<uint4*>(rb.frame);
