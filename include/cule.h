@@ -101,6 +101,18 @@ int cule_reset(cule_env* env, uint64_t seed, void* d_obs, void* cuda_stream);
 int cule_step(cule_env* env, const uint8_t* d_actions, void* d_obs, int32_t* d_rewards,
               uint8_t* d_dones, void* cuda_stream);
 
+/* Inference path (R#32), GRAY84 only.  d_stack is a DEVICE
+ * frame stack u8[N][4][84][84]: per env a ring of the last four observations of its current
+ * episode.  cule_reset_stacked: as cule_reset, with the reset observation in all four slots.
+ * cule_step_stacked: as cule_step, writing each env's observation into slot `slot` (0..3; the
+ * caller rotates it, so slots slot+1, slot+2, slot+3, slot (mod 4) run oldest to newest); an env
+ * whose step ended the episode (d_dones[i] = 1) is reset from the cache (R#20) and gets that
+ * entry's start observation in all four slots instead (its terminal observation is not
+ * returned).  CULE_E_INVAL for RAW handles, a slot outside [0, 3] or NULL buffers.  Async. */
+int cule_reset_stacked(cule_env* env, uint64_t seed, uint8_t* d_stack, void* cuda_stream);
+int cule_step_stacked(cule_env* env, const uint8_t* d_actions, uint8_t* d_stack, int slot,
+                      int32_t* d_rewards, uint8_t* d_dones, void* cuda_stream);
+
 /* Same as cule_step but with HOST buffers: copies h_actions in, steps, copies obs/rewards/
  * dones out through the workspace's I/O staging area; synchronises cuda_stream before
  * returning.  h_obs may be NULL (observations stay on the device). */

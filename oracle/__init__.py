@@ -71,6 +71,8 @@ def lib():
         L.orc_set_env_ids.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
         L.orc_reset.argtypes = [ctypes.c_void_p, ctypes.c_uint64, u8p]
         L.orc_step.argtypes = [ctypes.c_void_p, u8p, u8p, ctypes.POINTER(ctypes.c_int32), u8p]
+        L.orc_reset_stacked.argtypes = [ctypes.c_void_p, ctypes.c_uint64, u8p]
+        L.orc_step_stacked.argtypes = [ctypes.c_void_p, u8p, u8p, ctypes.c_int, ctypes.POINTER(ctypes.c_int32), u8p]
         L.orc_get_state.argtypes = [ctypes.c_void_p, u8p]
         L.orc_set_state.argtypes = [ctypes.c_void_p, u8p]
         L.orc_counters.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
@@ -176,6 +178,23 @@ class OracleEnv:
         lib().orc_step(self.h, _u8(a), _u8(obs), rew.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                        _u8(done))
         return obs, rew, done
+
+    # frame stack of the inference path (GRAY84; R#32)
+    def reset_stacked(self, seed: int = 0) -> np.ndarray:
+        stack = np.zeros((self.num_envs, 4) + self.obs_shape, np.uint8)
+        lib().orc_reset_stacked(self.h, seed, _u8(stack))
+        return stack
+
+    def step_stacked(self, actions, stack: np.ndarray, slot: int):
+        """One step; `stack` (u8[N][4][84][84]) is updated in place."""
+        assert stack.flags.c_contiguous and stack.shape == (self.num_envs, 4) + self.obs_shape
+        a = np.ascontiguousarray(actions, dtype=np.uint8)
+        rew = np.zeros(self.num_envs, np.int32)
+        done = np.zeros(self.num_envs, np.uint8)
+        rc = lib().orc_step_stacked(self.h, _u8(a), _u8(stack), slot,
+                                    rew.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _u8(done))
+        assert rc == 0
+        return rew, done
 
     def get_state(self) -> np.ndarray:
         s = np.zeros((self.num_envs, STATE_BYTES), np.uint8)

@@ -1194,6 +1194,44 @@ int orc_step(orc_env* e, const uint8_t* actions, uint8_t* obs, int32_t* rewards,
   return 0;
 }
 
+/* Frame stack of the inference path (R#32), GRAY84 only:
+ * stack = u8[N][4][84][84], a ring of the last four observations of each env's current
+ * episode.  orc_reset_stacked fills all four slots of every env with its reset observation;
+ * orc_step_stacked runs one step, then writes each env's observation into slot `slot`, except
+ * for an env whose step ended the episode: it was reset from the cache entry picked for its
+ * next episode, and all four of its slots get that entry's stored observation. */
+int orc_reset_stacked(orc_env* e, uint64_t seed, uint8_t* stack) {
+  size_t ob = (size_t)e->obs_bytes;
+  uint8_t* obs = (uint8_t*)malloc((size_t)e->num_envs * ob);
+  orc_reset(e, seed, obs);
+  for (int i = 0; i < e->num_envs; i++)
+    for (int k = 0; k < 4; k++) memcpy(stack + ((size_t)i * 4 + k) * ob, obs + (size_t)i * ob, ob);
+  free(obs);
+  return 0;
+}
+
+int orc_step_stacked(orc_env* e, const uint8_t* actions, uint8_t* stack, int slot, int32_t* rewards,
+                     uint8_t* dones) {
+  size_t ob = (size_t)e->obs_bytes;
+  if (slot < 0 || slot > 3) return -1;
+  uint8_t* obs = (uint8_t*)malloc((size_t)e->num_envs * ob);
+  orc_step(e, actions, obs, rewards, dones);
+  for (int i = 0; i < e->num_envs; i++) {
+    if (!dones[i]) {
+      memcpy(stack + ((size_t)i * 4 + slot) * ob, obs + (size_t)i * ob, ob);
+    } else {
+      /* the env now holds the cache entry of its next episode (episode index from its state) */
+      const uint8_t* s = e->states + (size_t)i * ORC_STATE_BYTES;
+      uint32_t ep = (uint32_t)s[196] | ((uint32_t)s[197] << 8) | ((uint32_t)s[198] << 16) | ((uint32_t)s[199] << 24);
+      int64_t g = e->gids[i];
+      size_t idx = (size_t)rom_of(e, g) * e->cfg.reset_cache_size + pick(e, g, ep);
+      for (int k = 0; k < 4; k++) memcpy(stack + ((size_t)i * 4 + k) * ob, e->cache_obs + idx * ob, ob);
+    }
+  }
+  free(obs);
+  return 0;
+}
+
 int orc_get_state(orc_env* e, uint8_t* states) {
   memcpy(states, e->states, (size_t)e->num_envs * ORC_STATE_BYTES);
   return 0;

@@ -76,6 +76,10 @@ orc_env* orc_create(const uint8_t* const* roms, const size_t* rom_lens, int n_ro
 int orc_set_env_ids(orc_env* e, const int64_t* gids);
 int orc_reset(orc_env* e, uint64_t seed, uint8_t* obs);
 int orc_step(orc_env* e, const uint8_t* actions, uint8_t* obs, int32_t* rewards, uint8_t* dones);
+/* frame stack of the inference path (GRAY84; stack = u8[N][4][84][84]; R#32) */
+int orc_reset_stacked(orc_env* e, uint64_t seed, uint8_t* stack);
+int orc_step_stacked(orc_env* e, const uint8_t* actions, uint8_t* stack, int slot, int32_t* rewards,
+                     uint8_t* dones);
 int orc_get_state(orc_env* e, uint8_t* states);
 int orc_set_state(orc_env* e, const uint8_t* states);
 int orc_counters(orc_env* e, int64_t* counters4);

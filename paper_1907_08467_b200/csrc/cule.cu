@@ -133,6 +133,9 @@ static cule::Params base_params(const cule_env* e) {
   p.srec = reinterpret_cast<const uint64_t*>(e->ws + e->L.srec);
   p.use_rec = e->use_rec;
   p.tickets = reinterpret_cast<unsigned int*>(e->ws + e->L.tickets);
+  p.obs_stride = (uint32_t)obs_bytes_of(e->cfg.obs_mode);
+  p.stacked = 0u;
+  p.stack_slot = 0u;
   for (int r = 0; r < 4; ++r) { p.slot_start[r] = e->slot_start[r]; p.first_env[r] = e->first_env[r]; }
   return p;
 }
@@ -389,16 +392,35 @@ int cule_reset(cule_env* e, uint64_t seed, void* d_obs, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint32_t blocks = ((uint32_t)e->N + 255) / 256;
   cule::reset_kernel<<<blocks, 256, 0, s>>>(p, (uint32_t)obs_bytes_of(e->cfg.obs_mode),
-                                            static_cast<uint8_t*>(d_obs), e->ws + e->L.cobs);
+                                            static_cast<uint8_t*>(d_obs), e->ws + e->L.cobs, 1u);
+  cudaMemsetAsync(e->ws + e->L.counters, 0, 32, s);
+  return cuda_check("reset_kernel");
+}
+
+int cule_reset_stacked(cule_env* e, uint64_t seed, uint8_t* d_stack, void* stream) {
+  CHECK_LIVE(e);
+  if (e->cfg.obs_mode != CULE_OBS_GRAY84) return fail(CULE_E_INVAL, "frame stacks need GRAY84 observations");
+  if (!d_stack) return fail(CULE_E_INVAL, "null buffer");
+  e->pick_seed = seed;
+  cule::Params p = base_params(e);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t blocks = ((uint32_t)e->N + 255) / 256;
+  cule::reset_kernel<<<blocks, 256, 0, s>>>(p, (uint32_t)cule::kObs84, d_stack, e->ws + e->L.cobs, 4u);
   cudaMemsetAsync(e->ws + e->L.counters, 0, 32, s);
   return cuda_check("reset_kernel");
 }
 
 static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32_t* d_rewards,
-                       uint8_t* d_dones, cudaStream_t s) {
+                       uint8_t* d_dones, cudaStream_t s, int stack_slot = -1) {
   cule::Params p = base_params(e);
   p.actions = d_actions;
   p.obs = static_cast<uint8_t*>(d_obs);
+  if (stack_slot >= 0) {  // frame stack: observation into slot `stack_slot` of u8[N][4][84][84]
+    p.stacked = 1u;
+    p.stack_slot = (uint32_t)stack_slot;
+    p.obs_stride = 4u * cule::kObs84;
+    p.obs += (size_t)stack_slot * cule::kObs84;
+  }
   p.rewards = d_rewards;
   p.dones = d_dones;
   if (e->engine == 1) {
@@ -418,6 +440,15 @@ int cule_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32_t* d_rew
   CHECK_LIVE(e);
   if (!d_actions || !d_obs || !d_rewards || !d_dones) return fail(CULE_E_INVAL, "null buffer");
   return launch_step(e, d_actions, d_obs, d_rewards, d_dones, static_cast<cudaStream_t>(stream));
+}
+
+int cule_step_stacked(cule_env* e, const uint8_t* d_actions, uint8_t* d_stack, int slot, int32_t* d_rewards,
+                      uint8_t* d_dones, void* stream) {
+  CHECK_LIVE(e);
+  if (e->cfg.obs_mode != CULE_OBS_GRAY84) return fail(CULE_E_INVAL, "frame stacks need GRAY84 observations");
+  if (!d_actions || !d_stack || !d_rewards || !d_dones) return fail(CULE_E_INVAL, "null buffer");
+  if (slot < 0 || slot > 3) return fail(CULE_E_INVAL, "stack slot must be in [0, 3]");
+  return launch_step(e, d_actions, d_stack, d_rewards, d_dones, static_cast<cudaStream_t>(stream), slot);
 }
 
 int cule_step_host(cule_env* e, const uint8_t* h_actions, void* h_obs, int32_t* h_rewards,

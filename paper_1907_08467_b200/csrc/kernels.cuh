@@ -67,7 +67,21 @@ struct Params {
   const uint64_t* srec;     // pre-decoded cartridge records, one per ROM image byte (scalar_predecode.h)
   uint32_t use_rec;         // records staged into shared memory (they fit)
   unsigned int* tickets;    // [2] env-slot ticket counter and finished-warp counter (self-resetting)
+  // GRAY84 observation placement: env i's observation at obs + i * obs_stride.  Frame stack
+  // (inference path, R#32): obs = stack + slot * 7056, obs_stride = 4 * 7056, and an
+  // env whose step ended the episode gets its new start observation in all four slots
+  uint32_t obs_stride;
+  uint32_t stacked, stack_slot;
 };
+
+// frame stack: all four slots of env i <- the cached start observation of entry ent
+__device__ __forceinline__ void stack_fill(const Params& p, uint32_t i, uint32_t ent, uint32_t lane) {
+  constexpr uint32_t kQ = (uint32_t)kObs84 / 16u;  // 441 16-byte chunks per observation
+  uint8_t* base = p.obs - (size_t)p.stack_slot * kObs84 + (size_t)i * p.obs_stride;
+  const uint4* src = reinterpret_cast<const uint4*>(p.cache_obs_out + (size_t)ent * kObs84);
+  for (uint32_t q = lane; q < 4u * kQ; q += 32u)
+    reinterpret_cast<uint4*>(base + (q / kQ) * kObs84)[q % kQ] = src[q % kQ];
+}
 
 // The env a thread emulates.  Envs are laid out so that the lanes of a warp run the same ROM
 // (g % n_roms), and at most `epw` lanes of a warp are used: at low env counts fewer envs per
@@ -390,7 +404,7 @@ __global__ void __launch_bounds__(128, CULE_MINB) step_kernel(Params p) {
     frame_out = kGray ? p.staging + (size_t)i * (2 * kFrameBytes) : p.obs + (size_t)i * kFrameBytes;
   }
   const int32_t status = simulate<kGray, false>(m, c, active, p.fs, frame_out, &episode_frames, 0);
-  uint32_t fault = 0, done = 0, ep_ret_done = 0;
+  uint32_t fault = 0, done = 0, ep_ret_done = 0, ent_done = 0;
   if (active) {
     fault = status == RUN_FRAME ? 0u : (uint32_t)status;
     m.fault = fault;
@@ -424,6 +438,7 @@ __global__ void __launch_bounds__(128, CULE_MINB) step_kernel(Params p) {
         st[q * N + i] = v;
       }
       st[12 * N + i] = make_uint4(0u, e, 0u, (uint32_t)p.cache_score[ent]);
+      ent_done = ent;
     }
   }
   // a8: counters (warp-aggregated)
@@ -442,8 +457,11 @@ __global__ void __launch_bounds__(128, CULE_MINB) step_kernel(Params p) {
     if (!((amask >> l) & 1u)) continue;
     const uint32_t env = __shfl_sync(kFull, i, l);
     const uint32_t f = __shfl_sync(kFull, fault, l);
-    if (kGray) {
-      uint8_t* o = p.obs + (size_t)env * kObs84;
+    const uint32_t dn = __shfl_sync(kFull, done, l), en = __shfl_sync(kFull, ent_done, l);
+    if (kGray && p.stacked && dn) {
+      stack_fill(p, env, en, lane);
+    } else if (kGray) {
+      uint8_t* o = p.obs + (size_t)env * p.obs_stride;
       if (f) warp_zero(o, kObs84, lane);
       else {
         const uint8_t* pair = p.staging + (size_t)env * (2 * kFrameBytes);
@@ -553,7 +571,7 @@ __global__ void __launch_bounds__(128) cache_kernel(Params p) {
 }
 
 // ---- reset: every env <- cache[rom(g)][pick(seed, g, 0)] ----------------------------------------
-__global__ void reset_kernel(Params p, uint32_t obs_bytes, uint8_t* d_obs, const uint8_t* cache_obs) {
+__global__ void reset_kernel(Params p, uint32_t obs_bytes, uint8_t* d_obs, const uint8_t* cache_obs, uint32_t copies) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.N) return;
   const size_t N = p.N;
@@ -570,10 +588,12 @@ __global__ void reset_kernel(Params p, uint32_t obs_bytes, uint8_t* d_obs, const
   }
   st[12 * N + i] = make_uint4(0u, 0u, 0u, (uint32_t)p.cache_score[ent]);
   for (int q = 13; q < 16; ++q) st[q * N + i] = make_uint4(0, 0, 0, 0);
-  if (d_obs) {
+  if (d_obs) {  // `copies` consecutive copies per env (4: every slot of a frame stack)
     const uint4* src = reinterpret_cast<const uint4*>(cache_obs + (size_t)ent * obs_bytes);
-    uint4* dst = reinterpret_cast<uint4*>(d_obs + (size_t)i * obs_bytes);
-    for (uint32_t q = 0; q < obs_bytes / 16u; ++q) dst[q] = src[q];
+    for (uint32_t k = 0; k < copies; ++k) {
+      uint4* dst = reinterpret_cast<uint4*>(d_obs + ((size_t)i * copies + k) * obs_bytes);
+      for (uint32_t q = 0; q < obs_bytes / 16u; ++q) dst[q] = src[q];
+    }
   }
 }
 

@@ -256,7 +256,7 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
   __syncwarp();
   uint8_t* frame_out = kDebug ? nullptr
                               : (kGray ? p.staging + (size_t)i * (2 * kFrameBytes) : p.obs + (size_t)i * kFrameBytes);
-  uint8_t* obs84 = (kGray && !kDebug) ? p.obs + (size_t)i * kObs84 : nullptr;
+  uint8_t* obs84 = (kGray && !kDebug) ? p.obs + (size_t)i * p.obs_stride : nullptr;
   const int32_t status = simulate_s<kGray, kDebug>(M, rom_all, dtab, ram, lg, tw, 76u * p.line_cap, lane,
                                                    kDebug ? 1u : p.fs, frame_out, episode_frames, p.debug_instr,
                                                    p.ystart, gray, rec_s, obs84, wb + kSOffRing,
@@ -320,9 +320,11 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
     st[lane * N + i] = v;
   }
   // a5: observation (GRAY84: already reduced row by row while frame fs was drawn; a faulted
-  // env's is zero)
+  // env's is zero; frame stack: an env that ended its episode gets its new start observation
+  // in all four slots)
   if (kGray) {
-    if (fault) warp_zero(p.obs + (size_t)i * kObs84, kObs84, lane);
+    if (p.stacked && done) stack_fill(p, i, ent, lane);
+    else if (fault) warp_zero(p.obs + (size_t)i * p.obs_stride, kObs84, lane);
   } else if (fault) {
     warp_zero(p.obs + (size_t)i * kFrameBytes, kFrameBytes, lane);
   }

@@ -88,6 +88,38 @@ class Env:
                                          ctypes.c_void_p(_stream_ptr(stream))))
         return self.obs, self.rewards, self.dones
 
+    # -- inference path: frame stack (R#32) ------------------
+    def new_stack(self) -> torch.Tensor:
+        """A device frame stack u8[N, 4, 84, 84] for reset_stacked / step_stacked."""
+        if self.obs_mode != "gray84":
+            raise ValueError("frame stacks need gray84 observations")
+        return torch.zeros((self.num_envs, 4, 84, 84), dtype=torch.uint8, device=self.device)
+
+    def reset_stacked(self, stack: torch.Tensor, seed: int = 0, stream=None) -> torch.Tensor:
+        self._check_stack(stack)
+        _lib.check(_lib.load().cule_reset_stacked(self._h, seed, ctypes.c_void_p(stack.data_ptr()),
+                                                  ctypes.c_void_p(_stream_ptr(stream))))
+        return stack
+
+    def step_stacked(self, actions: torch.Tensor, stack: torch.Tensor, slot: int, stream=None):
+        """One step writing each env's observation into stack[:, slot] (slot rotates 0..3); an env
+        that ended its episode gets its new start observation in all four slots."""
+        self._check_stack(stack)
+        if actions.dtype != torch.uint8 or actions.device != self.device or actions.numel() != self.num_envs:
+            raise ValueError("actions must be a uint8 tensor of N elements on the env's device")
+        actions = actions.contiguous()
+        _lib.check(_lib.load().cule_step_stacked(self._h, ctypes.c_void_p(actions.data_ptr()),
+                                                 ctypes.c_void_p(stack.data_ptr()), int(slot),
+                                                 ctypes.c_void_p(self.rewards.data_ptr()),
+                                                 ctypes.c_void_p(self.dones.data_ptr()),
+                                                 ctypes.c_void_p(_stream_ptr(stream))))
+        return self.rewards, self.dones
+
+    def _check_stack(self, stack: torch.Tensor) -> None:
+        if (stack.dtype != torch.uint8 or stack.device != self.device or not stack.is_contiguous()
+                or tuple(stack.shape) != (self.num_envs, 4, 84, 84)):
+            raise ValueError("stack must be a contiguous uint8 tensor [N, 4, 84, 84] on the env's device")
+
     def step_host(self, h_actions: torch.Tensor, h_obs, h_rewards: torch.Tensor,
                   h_dones: torch.Tensor, stream=None):
         """Host-buffer step (pinned CPU tensors): copies in, steps, copies out, synchronises."""

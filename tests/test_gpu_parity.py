@@ -339,3 +339,35 @@ def test_sampled_parity_at_cfg2_size():
         assert (o.cpu().numpy()[sample] == o2).all() and (r.cpu().numpy()[sample] == r2).all()
         assert (d.cpu().numpy()[sample] == d2).all()
     assert_same_state(gpu.get_state()[sample], ref.get_state(), "cfg2 sample")
+
+
+@pytest.mark.parametrize("roms", [["R1"], ["R1", "R2", "R3", "R4"]])
+def test_frame_stack_parity(roms):
+    """Inference path (R#32): the device frame stack
+    u8[N][4][84][84] after cule_reset_stacked and every cule_step_stacked equals the oracle's,
+    bit for bit, with episode ends (an 8-frame cap plus the games' own terminals) on every env."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    rl = [games.build_rom(n) for n in roms]
+    n = 70
+    cfg = dict(reset_cache_size=5, max_episode_frames=8 * 4 + 4)
+    gpu = Env(rl, n, 4, **cfg)
+    check_engine(gpu)
+    ref = oracle.OracleEnv(rl, n, 4, H.palette_rgb(), obs_mode=1, **cfg)
+    stack = gpu.new_stack()
+    gpu.reset_stacked(stack, 11)
+    rstack = ref.reset_stacked(11)
+    assert (stack.cpu().numpy() == rstack).all(), "reset stacks differ"
+    acts = H.random_actions(n, 25, 99)
+    n_done = 0
+    for t in range(25):
+        r, d = gpu.step_stacked(torch.from_numpy(acts[t]).cuda(), stack, t % 4)
+        r2, d2 = ref.step_stacked(acts[t], rstack, t % 4)
+        assert (r.cpu().numpy() == r2).all() and (d.cpu().numpy() == d2).all(), t
+        s = stack.cpu().numpy()
+        if not (s == rstack).all():
+            bad = np.nonzero((s != rstack).reshape(n, -1).any(1))[0]
+            raise AssertionError(f"step {t}: stacks differ for envs {bad[:8].tolist()}")
+        n_done += int(d2.sum())
+    assert_same_state(gpu.get_state(), ref.get_state(), "end")
+    assert n_done >= n
