@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--inference-steps", type=int, default=60,
+                    help="steps of the inference-path measurement (0: skip; gray84 configs only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-envs", type=int, default=16)
     ap.add_argument("--cpu-sample-steps", type=int, default=100)
@@ -208,6 +210,69 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------------------------
 # the CUDA arm
 # ---------------------------------------------------------------------------------------------
+class NatureCNN:
+    """The DQN/A2C Atari policy trunk (conv 8x8/4 32, 4x4/2 64, 3x3/1 64, fc 512, 18 logits),
+    random init, bf16: the consumer of the frame stack for the inference-path measurement (plain
+    PyTorch: the policy is not part of the emulation hot path)."""
+
+    def __init__(self, dev):
+        import torch
+        g = torch.Generator(device="cpu").manual_seed(7)
+        def p(*shape, fan):
+            return (torch.randn(*shape, generator=g) / fan ** 0.5).to(dev, torch.bfloat16)
+        self.w1, self.b1 = p(32, 4, 8, 8, fan=256), torch.zeros(32, device=dev, dtype=torch.bfloat16)
+        self.w2, self.b2 = p(64, 32, 4, 4, fan=512), torch.zeros(64, device=dev, dtype=torch.bfloat16)
+        self.w3, self.b3 = p(64, 64, 3, 3, fan=576), torch.zeros(64, device=dev, dtype=torch.bfloat16)
+        self.w4, self.b4 = p(512, 3136, fan=3136), torch.zeros(512, device=dev, dtype=torch.bfloat16)
+        self.w5, self.b5 = p(18, 512, fan=512), torch.zeros(18, device=dev, dtype=torch.bfloat16)
+
+    def act(self, stack, slot, gen):
+        """Sample actions from the stack as the step kernel left it: slot `slot` is the newest
+        frame, so conv1's input channels are permuted instead of the frames (no copy)."""
+        import torch
+        import torch.nn.functional as F
+        order = [(slot + 1 + k) % 4 for k in range(4)]      # oldest -> newest ring slots
+        inv = [order.index(c) for c in range(4)]             # ring slot c holds temporal frame inv[c]
+        x = stack.to(torch.bfloat16).mul_(1.0 / 255.0)
+        h = F.relu(F.conv2d(x, self.w1[:, inv], self.b1, stride=4))
+        h = F.relu(F.conv2d(h, self.w2, self.b2, stride=2))
+        h = F.relu(F.conv2d(h, self.w3, self.b3, stride=1))
+        h = F.relu(F.linear(h.flatten(1), self.w4, self.b4))
+        logits = F.linear(h, self.w5, self.b5).float()
+        return torch.multinomial(torch.softmax(logits, -1), 1, generator=gen).squeeze(1).to(torch.uint8)
+
+
+def run_inference(env, dev, envs, world, fs, steps, rank):
+    import torch
+
+    from paper_1907_08467_b200 import dist as D
+    pol = NatureCNN(dev)
+    stack = env.new_stack()
+    env.reset_stacked(stack, 5)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77 + rank)
+    slot = 0
+    for t in range(3):  # warm-up (cuDNN algorithm choice)
+        a = pol.act(stack, (slot - 1) % 4, gen)
+        env.step_stacked(a, stack, slot)
+        slot = (slot + 1) % 4
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for t in range(steps):
+        a = pol.act(stack, (slot - 1) % 4, gen)
+        env.step_stacked(a, stack, slot)
+        slot = (slot + 1) % 4
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    ms = D.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    return {"value": envs * world * fs * steps / (ms / 1000.0), "unit": "frames/s",
+            "ms_per_step": ms / steps, "steps": steps,
+            "loop": "frame stack u8[N,4,84,84] written by the step kernel -> Nature-CNN policy (bf16, "
+                    "random init, torch) -> device-side multinomial sampling -> next step",
+            "gpu_launches_per_step": "1 emulation kernel + the policy's torch kernels"}
+
+
 def run_cule(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -278,6 +343,12 @@ def run_cule(args, rank, world, local_rank):
     e_dt = D.max_over_ranks(time.perf_counter() - e0, device=dev)
     e2e_fps = envs * world * fs * args.e2e_steps / e_dt
 
+    # inference path: frame stack written by the step kernel, a small
+    # random-init policy reading it in place, device-side action sampling; emulated frames/s
+    inference = None
+    if args.inference_steps > 0 and mode == "gray84" and not args.envs:
+        inference = run_inference(env, dev, envs, world, fs, args.inference_steps, rank)
+
     if rank != 0:
         return
     # roofline of the dominant (only) kernel: the step kernel, one launch per step
@@ -315,6 +386,7 @@ def run_cule(args, rank, world, local_rank):
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": envs,
                 "d2h_bytes_per_step": envs * (ob + 4 + 1)},
         "gpu_launches": K,
+        "inference": inference,
         "roofline": roof,
         "clocks": clk,
         "counters": {"frames": int(counters[0]), "episodes": int(counters[1]),
