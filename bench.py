@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--vtrace", type=int, default=1, choices=[0, 1],
+                    help="also time the batched V-trace kernel (NEXT-3)")
     ap.add_argument("--inference-steps", type=int, default=60,
                     help="steps of the inference-path measurement (0: skip; gray84 configs only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -273,6 +275,43 @@ def run_inference(env, dev, envs, world, fs, steps, rank):
             "gpu_launches_per_step": "1 emulation kernel + the policy's torch kernels"}
 
 
+def run_vtrace(dev, pk):
+    """Batched V-trace targets (NEXT-3, cule_vtrace): time-major fp32 [T][B], one thread per
+    trajectory; a pure HBM stream of 29 bytes per (t, b) (r, V, log mu, log pi: 4 B each in,
+    done 1 B in; v, rho, advantage: 4 B each out) + 4 B per bootstrap.  Timed with CUDA events
+    over 50 back-to-back launches, inputs resident in HBM; reported at the training shape of
+    the bench config (T=20 steps, B=4096) and at B=2^20 (the HBM roofline shape)."""
+    import torch
+
+    from paper_1907_08467_b200.vtrace import vtrace
+    out = {}
+    for T, B in ((20, 4096), (20, 1 << 20)):
+        g = torch.Generator(device=dev)
+        g.manual_seed(3)
+        r = torch.randn(T, B, device=dev, generator=g)
+        V = torch.randn(T, B, device=dev, generator=g)
+        vb = torch.randn(B, device=dev, generator=g)
+        lm = torch.randn(T, B, device=dev, generator=g) * 0.5
+        lp = torch.randn(T, B, device=dev, generator=g) * 0.5
+        d = (torch.rand(T, B, device=dev, generator=g) < 0.05).to(torch.uint8)
+        for _ in range(3):
+            vtrace(r, V, vb, lm, lp, d, 0.99)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(50):
+            vtrace(r, V, vb, lm, lp, d, 0.99)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        s = e0.elapsed_time(e1) / 1000.0 / 50
+        nbytes = T * B * 29 + 4 * B
+        out[f"T{T}_B{B}"] = {"us_per_launch": s * 1e6, "achieved_gbs": nbytes / s / 1e9,
+                             "frac_hbm": nbytes / s / 1e9 / pk["hbm_gbs"], "bytes_per_launch": nbytes,
+                             "trajectories_per_s": B / s}
+    out["roofline"] = {"bound": "hbm", "peak_gbs": pk["hbm_gbs"], "peak_source": pk["source"]}
+    return out
+
+
 def run_cule(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -392,6 +431,8 @@ def run_cule(args, rank, world, local_rank):
         "counters": {"frames": int(counters[0]), "episodes": int(counters[1]),
                      "return_sum": int(counters[2]), "faults": int(counters[3])},
     }
+    if args.vtrace:
+        line["vtrace"] = run_vtrace(dev, pk)
     if not args.no_cpu_baseline and world == 1:
         cores = host_cores()
         procs = max(1, min(cores, 64))

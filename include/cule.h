@@ -113,6 +113,18 @@ int cule_reset_stacked(cule_env* env, uint64_t seed, uint8_t* d_stack, void* cud
 int cule_step_stacked(cule_env* env, const uint8_t* d_actions, uint8_t* d_stack, int slot,
                       int32_t* d_rewards, uint8_t* d_dones, void* cuda_stream);
 
+/* Batched V-trace targets (Eq. target.off computed
+ * by the recursive form, Eqs. rho / c truncated importance weights).  All arrays are DEVICE
+ * memory, time-major [T][B] (step t of trajectory b at t*B + b), fp32; d_bootstrap is [B]
+ * (V(s_T)); d_dones[t][b] = 1 marks a terminal at step t, which stops bootstrapping through it
+ * (gamma_t = 0; R#33).  Outputs: d_vs[T][B] = v_t, d_rho[T][B] = rho_t =
+ * min(rho_bar, pi/mu), d_adv[T][B] = r_t + gamma_t v_{t+1} - V(s_t) (v_T = bootstrap).
+ * CULE_E_INVAL for NULL buffers, T or B <= 0, gamma outside (0, 1] or not rho_bar >= c_bar > 0.
+ * Async on cuda_stream; needs no env handle. */
+int cule_vtrace(const float* d_rewards, const float* d_values, const float* d_bootstrap, const float* d_log_mu,
+                const float* d_log_pi, const uint8_t* d_dones, int T, int B, float gamma, float rho_bar,
+                float c_bar, float* d_vs, float* d_rho, float* d_adv, void* cuda_stream);
+
 /* Same as cule_step but with HOST buffers: copies h_actions in, steps, copies obs/rewards/
  * dones out through the workspace's I/O staging area; synchronises cuda_stream before
  * returning.  h_obs may be NULL (observations stay on the device). */

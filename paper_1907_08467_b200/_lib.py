@@ -26,7 +26,7 @@ STATE_BYTES = 256
 EXPORTS = ["cule_default_config", "cule_workspace_bytes", "cule_create", "cule_reset",
            "cule_step", "cule_step_host", "cule_get_state", "cule_set_state", "cule_counters",
            "cule_debug_exec", "cule_num_envs", "cule_frameskip", "cule_obs_bytes",
-           "cule_engine", "cule_reset_stacked", "cule_step_stacked", "cule_destroy", "cule_last_error"]
+           "cule_engine", "cule_reset_stacked", "cule_step_stacked", "cule_vtrace", "cule_destroy", "cule_last_error"]
 
 
 class CuleConfig(ctypes.Structure):
@@ -69,6 +69,8 @@ def load():
     L.cule_step.argtypes = [vp, vp, vp, vp, vp, vp]
     L.cule_step_host.argtypes = [vp, vp, vp, vp, vp, vp]
     L.cule_reset_stacked.argtypes = [vp, ctypes.c_uint64, vp, vp]
+    f32 = ctypes.c_float
+    L.cule_vtrace.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, f32, f32, f32, vp, vp, vp, vp]
     L.cule_step_stacked.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp, vp]
     L.cule_get_state.argtypes = [vp, vp, vp]
     L.cule_set_state.argtypes = [vp, vp, vp]
@@ -83,7 +85,7 @@ def load():
     L.cule_last_error.argtypes = []
     L.cule_last_error.restype = ctypes.c_char_p
     for name in ("cule_create", "cule_reset", "cule_step", "cule_step_host", "cule_get_state",
-                 "cule_reset_stacked", "cule_step_stacked",
+                 "cule_reset_stacked", "cule_step_stacked", "cule_vtrace",
                  "cule_set_state", "cule_counters", "cule_debug_exec", "cule_num_envs",
                  "cule_frameskip", "cule_engine", "cule_destroy"):
         getattr(L, name).restype = ctypes.c_int

@@ -19,6 +19,7 @@
 #include "scalar_decode.h"
 #include "scalar_predecode.h"
 #include "scalar_kernels.cuh"
+#include "vtrace.cuh"
 
 namespace {
 
@@ -514,6 +515,21 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
     cule::debug_kernel<<<e->grid, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);
   }
   return cuda_check("debug_kernel");
+}
+
+int cule_vtrace(const float* d_rewards, const float* d_values, const float* d_bootstrap, const float* d_log_mu,
+                const float* d_log_pi, const uint8_t* d_dones, int T, int B, float gamma, float rho_bar, float c_bar,
+                float* d_vs, float* d_rho, float* d_adv, void* stream) {
+  if (!d_rewards || !d_values || !d_bootstrap || !d_log_mu || !d_log_pi || !d_dones || !d_vs || !d_rho || !d_adv)
+    return fail(CULE_E_INVAL, "null buffer");
+  if (T <= 0 || B <= 0) return fail(CULE_E_INVAL, "T and B must be > 0");
+  if (!(gamma > 0.0f && gamma <= 1.0f)) return fail(CULE_E_INVAL, "gamma must be in (0, 1]");
+  if (!(c_bar > 0.0f && rho_bar >= c_bar)) return fail(CULE_E_INVAL, "need rho_bar >= c_bar > 0");
+  const uint32_t blocks = ((uint32_t)B + 255u) / 256u;
+  cule::vtrace_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_rewards, d_values, d_bootstrap, d_log_mu, d_log_pi, d_dones, (uint32_t)T, (uint32_t)B, gamma, rho_bar, c_bar,
+      d_vs, d_rho, d_adv);
+  return cuda_check("vtrace_kernel");
 }
 
 int cule_num_envs(const cule_env* e) { return live(e) ? e->N : CULE_E_CLOSED; }

@@ -1,0 +1,43 @@
+// vtrace.cuh — batched V-trace targets (Eqs.
+// target.off / rho / c and the recursive form "we compute the V-trace update recursively").
+//
+// One thread per trajectory (env) b, walking t = T-1 .. 0 with the recursive form
+//   v_t = V_t + delta_t + gamma_t c_t (v_{t+1} - V_{t+1}),   v_T = V_boot,
+//   delta_t = rho_t (r_t + gamma_t V_{t+1} - V_t),  rho_t = min(rho_bar, pi/mu), c_t = min(c_bar, pi/mu),
+// with gamma_t = gamma (1 - done_t) (a terminal at step t stops bootstrapping through it,
+// DESIGN.md R#33), and the policy-gradient advantage r_t + gamma_t v_{t+1} - V_t.  Arrays are
+// time-major [T][B], so a warp's 32 trajectories read and write 128 contiguous bytes per array
+// and step: the kernel is a pure HBM stream, fp32 in and out, fp32 arithmetic.
+#pragma once
+#include <stdint.h>
+
+namespace cule {
+
+__global__ void __launch_bounds__(256) vtrace_kernel(const float* __restrict__ r, const float* __restrict__ V,
+                                                     const float* __restrict__ V_boot,
+                                                     const float* __restrict__ log_mu,
+                                                     const float* __restrict__ log_pi,
+                                                     const uint8_t* __restrict__ done, uint32_t T, uint32_t B,
+                                                     float gamma, float rho_bar, float c_bar, float* __restrict__ vs,
+                                                     float* __restrict__ rho_out, float* __restrict__ adv) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float v_next = V_boot[b];  // v_{t+1}
+  float V_next = v_next;     // V(s_{t+1})
+  for (uint32_t k = T; k-- > 0;) {
+    const size_t o = (size_t)k * B + b;
+    const float ratio = expf(log_pi[o] - log_mu[o]);
+    const float rho = fminf(rho_bar, ratio), c = fminf(c_bar, ratio);
+    const float g = done[o] ? 0.0f : gamma;
+    const float Vt = V[o], rt = r[o];
+    const float delta = rho * (rt + g * V_next - Vt);
+    const float v = Vt + delta + g * c * (v_next - V_next);
+    vs[o] = v;
+    rho_out[o] = rho;
+    adv[o] = rt + g * v_next - Vt;
+    v_next = v;
+    V_next = Vt;
+  }
+}
+
+}  // namespace cule
