@@ -279,7 +279,7 @@ def run_vtrace(dev, pk):
     """Batched V-trace targets (NEXT-3, cule_vtrace): time-major fp32 [T][B], one thread per
     trajectory; a pure HBM stream of 29 bytes per (t, b) (r, V, log mu, log pi: 4 B each in,
     done 1 B in; v, rho, advantage: 4 B each out) + 4 B per bootstrap.  Timed with CUDA events
-    over 50 back-to-back launches, inputs resident in HBM; reported at the training shape of
+    over 50 launches replayed from one CUDA graph, inputs resident in HBM; reported at the training shape of
     the bench config (T=20 steps, B=4096) and at B=2^20 (the HBM roofline shape)."""
     import torch
 
@@ -294,13 +294,22 @@ def run_vtrace(dev, pk):
         lm = torch.randn(T, B, device=dev, generator=g) * 0.5
         lp = torch.randn(T, B, device=dev, generator=g) * 0.5
         d = (torch.rand(T, B, device=dev, generator=g) < 0.05).to(torch.uint8)
-        for _ in range(3):
-            vtrace(r, V, vb, lm, lp, d, 0.99)
+        bufs = (torch.empty_like(r), torch.empty_like(r), torch.empty_like(r))
+        side = torch.cuda.Stream(dev)
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                vtrace(r, V, vb, lm, lp, d, 0.99, out=bufs)
+        torch.cuda.synchronize(dev)
+        # 50 launches captured in one CUDA graph: the kernel's own time, not the host's call rate
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            for _ in range(50):
+                vtrace(r, V, vb, lm, lp, d, 0.99, out=bufs)
+        graph.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         e0.record()
-        for _ in range(50):
-            vtrace(r, V, vb, lm, lp, d, 0.99)
+        graph.replay()
         e1.record()
         torch.cuda.synchronize(dev)
         s = e0.elapsed_time(e1) / 1000.0 / 50

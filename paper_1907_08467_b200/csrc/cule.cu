@@ -525,8 +525,10 @@ int cule_vtrace(const float* d_rewards, const float* d_values, const float* d_bo
   if (T <= 0 || B <= 0) return fail(CULE_E_INVAL, "T and B must be > 0");
   if (!(gamma > 0.0f && gamma <= 1.0f)) return fail(CULE_E_INVAL, "gamma must be in (0, 1]");
   if (!(c_bar > 0.0f && rho_bar >= c_bar)) return fail(CULE_E_INVAL, "need rho_bar >= c_bar > 0");
-  const uint32_t blocks = ((uint32_t)B + 255u) / 256u;
-  cule::vtrace_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  // 64-thread blocks: a training-sized batch (thousands of trajectories) still spreads over
+  // the SMs, and each SM keeps many trajectories' loads in flight
+  const uint32_t blocks = ((uint32_t)B + 63u) / 64u;
+  cule::vtrace_kernel<<<blocks, 64, 0, static_cast<cudaStream_t>(stream)>>>(
       d_rewards, d_values, d_bootstrap, d_log_mu, d_log_pi, d_dones, (uint32_t)T, (uint32_t)B, gamma, rho_bar, c_bar,
       d_vs, d_rho, d_adv);
   return cuda_check("vtrace_kernel");

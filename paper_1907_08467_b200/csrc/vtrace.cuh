@@ -13,7 +13,7 @@
 
 namespace cule {
 
-__global__ void __launch_bounds__(256) vtrace_kernel(const float* __restrict__ r, const float* __restrict__ V,
+__global__ void __launch_bounds__(64) vtrace_kernel(const float* __restrict__ r, const float* __restrict__ V,
                                                      const float* __restrict__ V_boot,
                                                      const float* __restrict__ log_mu,
                                                      const float* __restrict__ log_pi,
@@ -24,19 +24,37 @@ __global__ void __launch_bounds__(256) vtrace_kernel(const float* __restrict__ r
   if (b >= B) return;
   float v_next = V_boot[b];  // v_{t+1}
   float V_next = v_next;     // V(s_{t+1})
-  for (uint32_t k = T; k-- > 0;) {
-    const size_t o = (size_t)k * B + b;
-    const float ratio = expf(log_pi[o] - log_mu[o]);
-    const float rho = fminf(rho_bar, ratio), c = fminf(c_bar, ratio);
-    const float g = done[o] ? 0.0f : gamma;
-    const float Vt = V[o], rt = r[o];
-    const float delta = rho * (rt + g * V_next - Vt);
-    const float v = Vt + delta + g * c * (v_next - V_next);
-    vs[o] = v;
-    rho_out[o] = rho;
-    adv[o] = rt + g * v_next - Vt;
-    v_next = v;
-    V_next = Vt;
+  // the recursion is sequential in t but its inputs are not: each chunk of kChunk steps is
+  // loaded first (all loads in flight together), then walked backwards
+  constexpr uint32_t kChunk = 8;
+  for (uint32_t hi = T; hi > 0;) {
+    const uint32_t lo = hi > kChunk ? hi - kChunk : 0u;
+    float rr[kChunk], vv[kChunk], lm[kChunk], lp[kChunk];
+    uint8_t dd[kChunk];
+#pragma unroll
+    for (uint32_t j = 0; j < kChunk; ++j) {
+      if (lo + j < hi) {
+        const size_t o = (size_t)(lo + j) * B + b;
+        rr[j] = r[o]; vv[j] = V[o]; lm[j] = log_mu[o]; lp[j] = log_pi[o]; dd[j] = done[o];
+      }
+    }
+#pragma unroll
+    for (int j = kChunk - 1; j >= 0; --j) {
+      if (lo + (uint32_t)j >= hi) continue;
+      const size_t o = (size_t)(lo + (uint32_t)j) * B + b;
+      const float ratio = expf(lp[j] - lm[j]);
+      const float rho = fminf(rho_bar, ratio), c = fminf(c_bar, ratio);
+      const float g = dd[j] ? 0.0f : gamma;
+      const float Vt = vv[j], rt = rr[j];
+      const float delta = rho * (rt + g * V_next - Vt);
+      const float v = Vt + delta + g * c * (v_next - V_next);
+      vs[o] = v;
+      rho_out[o] = rho;
+      adv[o] = rt + g * v_next - Vt;
+      v_next = v;
+      V_next = Vt;
+    }
+    hi = lo;
   }
 }
 
