@@ -385,20 +385,17 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   for (uint32_t ln = la; ln <= lb; ++ln) {
     const uint32_t xa = ln == l0 ? xa0 : 0u, xb = ln == l1 ? xb1 : 160u;
     if (xb <= xa) continue;
-    if (lane < 10u && xa < cx + 16u && xb > cx) {
-      const bool cb = (int32_t)ln == comb && lane == 0u;  // HMOVE comb: x < 8 black (R#11)
-      const uint32_t p0 = cb ? rb.fill : x0w, p1 = cb ? rb.fill : x1w;
-      if (xa <= cx && xb >= cx + 16u) {
-        rb.r0 = p0; rb.r1 = p1; rb.r2 = x2w; rb.r3 = x3w;
-      } else {
-        const uint32_t m0 = group_mask(cx, xa, xb), m1 = group_mask(cx + 4u, xa, xb),
-                       m2 = group_mask(cx + 8u, xa, xb), m3 = group_mask(cx + 12u, xa, xb);
-        rb.r0 = (rb.r0 & ~m0) | (p0 & m0);
-        rb.r1 = (rb.r1 & ~m1) | (p1 & m1);
-        rb.r2 = (rb.r2 & ~m2) | (x2w & m2);
-        rb.r3 = (rb.r3 & ~m3) | (x3w & m3);
-      }
-    }
+    // pixels [xa, xb) of this lane's chunk [cx, cx+16) as a 16-bit mask (0 for lanes >= 10),
+    // merged branch-free: bit k of the mask <-> byte k % 4 of word k / 4
+    const uint32_t a = xa > cx ? min(xa - cx, 16u) : 0u, b = xb > cx ? min(xb - cx, 16u) : 0u;
+    const uint32_t pm = b > a ? (0xFFFFu >> (16u - (b - a))) << a : 0u;
+    const bool cb = (int32_t)ln == comb && lane == 0u;  // HMOVE comb: x < 8 black (R#11)
+    const uint32_t p0 = cb ? rb.fill : x0w, p1 = cb ? rb.fill : x1w;
+    const uint32_t m0 = nib_bytes(pm), m1 = nib_bytes(pm >> 4), m2 = nib_bytes(pm >> 8), m3 = nib_bytes(pm >> 12);
+    rb.r0 = (rb.r0 & ~m0) | (p0 & m0);
+    rb.r1 = (rb.r1 & ~m1) | (p1 & m1);
+    rb.r2 = (rb.r2 & ~m2) | (x2w & m2);
+    rb.r3 = (rb.r3 & ~m3) | (x3w & m3);
     if (xb == 160u) row_done(rb, lane);
   }
 }
