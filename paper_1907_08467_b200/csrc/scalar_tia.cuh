@@ -277,6 +277,10 @@ __device__ __forceinline__ void fused_row(const RowBuf& rb, uint32_t lane) {
     uint4 m = make_uint4(rb.r0, rb.r1, rb.r2, rb.r3);
     if (rb.prev) {
       const uint4 q = reinterpret_cast<const uint4*>(rb.prev + r * 160u)[lane];
+      // frame fs-1 streams from L2/HBM one row per completed row: prefetch four rows ahead into
+      // L1 so the next rows' loads do not stall the replay
+      if (r + 4u < (uint32_t)kFrameH)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(rb.prev + (r + 4u) * 160u + 16u * lane));
       m.x = __vmaxu4(m.x, q.x); m.y = __vmaxu4(m.y, q.y); m.z = __vmaxu4(m.z, q.z); m.w = __vmaxu4(m.w, q.w);
     }
     asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rb.ring_s + slot * 160u + 16u * lane), "r"(m.x),
