@@ -393,6 +393,27 @@ def run_cule(args, rank, world, local_rank):
     e_dt = D.max_over_ranks(time.perf_counter() - e0, device=dev)
     e2e_fps = envs * world * fs * args.e2e_steps / e_dt
 
+    # variant (not the headline): the same workload with the exact idle-loop skip
+    variant = None
+    if not args.no_variant and not args.idle_skip and world == 1:
+        env2 = Env(roms, envs, fs, obs_mode=mode, env_index_base=base, device=dev, idle_skip=1)
+        env2.reset(0)
+        for t in range(W):
+            env2.step(acts[t])
+        torch.cuda.synchronize(dev)
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for t in range(W, W + K):
+            env2.step(acts[t])
+        v1.record(stream)
+        torch.cuda.synchronize(dev)
+        vms = v0.elapsed_time(v1)
+        variant = {"idle_skip": 1, "value": envs * fs * K / (vms / 1000.0), "unit": "frames/s",
+                   "ms_per_step": vms / K, "note": "exact closed-form skip of [timer read; branch back] "
+                                                   "poll loops (DESIGN.md §2 R#24); reported beside the "
+                                                   "headline, never as it"}
+        env2.close()
+
     # inference path: frame stack written by the step kernel, a small
     # random-init policy reading it in place, device-side action sampling; emulated frames/s
     inference = None
@@ -437,6 +458,7 @@ def run_cule(args, rank, world, local_rank):
                 "d2h_bytes_per_step": envs * (ob + 4 + 1)},
         "gpu_launches": K,
         "inference": inference,
+        "variant": variant,
         "roofline": roof,
         "clocks": clk,
         "counters": {"frames": int(counters[0]), "episodes": int(counters[1]),
