@@ -24,9 +24,6 @@ __device__ __forceinline__ uint32_t with_byte(uint32_t w, int i, uint32_t v) {
 //   w0 COLUP0 COLUP1 COLUPF COLUBK | w1 PF0 PF1 PF2 CTRLPF | w2 NUSIZ0 NUSIZ1 GRP0new GRP0old
 //   w3 GRP1new GRP1old HMP0 HMP1   | w4 HMM0 HMM1 HMBL     | w5 flags(16) comb_line(16)
 //   w6 posP0 posP1 posM0 posM1     | w7 posBL, collisions(16) << 16 | t = colour clock
-// write registers that change which objects are present (PF0-2, GRP0/1, ENAM0/1, ENABL,
-// VDELP0/1, VDELBL, RESMP0/1): the pairs that could still collide are recomputed after them
-constexpr uint64_t kPresenceRegs = (7ull << 0x0D) | (0x1Full << 0x1B) | (0x1Full << 0x25);
 
 // collision pairs two present objects can set, by presence bits (0 P0, 1 P1, 2 M0, 3 M1, 4 BL,
 // 5 PF) -> latch bits (bit 2r = D7, 2r+1 = D6 of read register r: CXM0P M0-P1/M0-P0, CXM1P
@@ -64,7 +61,8 @@ __constant__ DirtyTable kDirtyTable = DirtyTable();
 
 struct TiaP {
   uint32_t w0, w1, w2, w3, w4, w5, w6, w7, t;
-  uint32_t poss;  // cached possible_pairs(), 0xFFFFFFFF = stale (not kept in shared memory)
+  uint32_t pres;  // presence bits (0 P0, 1 P1, 2 M0, 3 M1, 4 BL, 5 PF), kept current by apply()
+                  // (not stored in shared memory: recomputed at load)
 
   __device__ __forceinline__ uint32_t f(int b) const { return (w5 >> b) & 1u; }
   __device__ __forceinline__ void setf(int b, uint32_t v) { w5 = (w5 & ~(1u << b)) | ((v & 1u) << b); }
@@ -72,7 +70,7 @@ struct TiaP {
   __device__ __forceinline__ int32_t comb_line() const { return (int32_t)(int16_t)(w5 >> 16); }
   __device__ __forceinline__ void load(const uint32_t* tw) {
     w0 = tw[0]; w1 = tw[1]; w2 = tw[2]; w3 = tw[3]; w4 = tw[4]; w5 = tw[5]; w6 = tw[6]; w7 = tw[7]; t = tw[8];
-    poss = 0xFFFFFFFFu;
+    pres = p0_on() | (p1_on() << 1) | (m0_on() << 2) | (m1_on() << 3) | (ball_on() << 4) | (pf_on() << 5);
   }
   __device__ __forceinline__ void store(uint32_t* tw) const {
     tw[0] = w0; tw[1] = w1; tw[2] = w2; tw[3] = w3; tw[4] = w4; tw[5] = w5; tw[6] = w6; tw[7] = w7; tw[8] = t;
@@ -81,18 +79,15 @@ struct TiaP {
   __device__ __forceinline__ uint32_t grp1() const { return byte_of(w3, f(8) ? 1 : 0); }
   __device__ __forceinline__ uint32_t ball_on() const { return f(9) ? f(6) : f(5); }
 
-  // collision latches the objects present now could still set (an absent object cannot collide)
-  __device__ __forceinline__ uint32_t open_pairs() {
-    if (poss == 0xFFFFFFFFu) poss = possible_pairs();
-    return poss & ~coll();
-  }
-  __device__ __forceinline__ uint32_t possible_pairs() const {
-    const uint32_t p0 = grp0() != 0u, p1 = grp1() != 0u;
-    const uint32_t m0 = f(3) & (f(10) ^ 1u), m1 = f(4) & (f(11) ^ 1u);
-    const uint32_t bl = ball_on();
-    const uint32_t pf = (w1 & 0x00FFFFF0u) != 0u;  // PF0 D4-D7, PF1, PF2
-    return kPairTable.v[p0 | (p1 << 1) | (m0 << 2) | (m1 << 3) | (bl << 4) | (pf << 5)];
-  }
+  // presence of each object (an absent object cannot collide)
+  __device__ __forceinline__ uint32_t p0_on() const { return grp0() != 0u ? 1u : 0u; }
+  __device__ __forceinline__ uint32_t p1_on() const { return grp1() != 0u ? 1u : 0u; }
+  __device__ __forceinline__ uint32_t m0_on() const { return f(3) & (f(10) ^ 1u); }
+  __device__ __forceinline__ uint32_t m1_on() const { return f(4) & (f(11) ^ 1u); }
+  __device__ __forceinline__ uint32_t pf_on() const { return (w1 & 0x00FFFFF0u) != 0u ? 1u : 0u; }  // PF0 D4-D7, PF1, PF2
+  __device__ __forceinline__ void set_pres(int b, uint32_t on) { pres = (pres & ~(1u << b)) | (on << b); }
+  // collision latches the objects present now could still set
+  __device__ __forceinline__ uint32_t open_pairs() const { return kPairTable.v[pres] & ~coll(); }
 
   // apply a logged write at colour clock T (DESIGN.md §2 R#7-R#12)
   __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T) {
@@ -104,7 +99,7 @@ struct TiaP {
       case 0x0A: w1 = with_byte(w1, 3, v); break;
       case 0x0B: setf(1, v >> 3); break;
       case 0x0C: setf(2, v >> 3); break;
-      case 0x0D: case 0x0E: case 0x0F: w1 = with_byte(w1, (int)(r - 0x0Du), v); break;
+      case 0x0D: case 0x0E: case 0x0F: w1 = with_byte(w1, (int)(r - 0x0Du), v); set_pres(5, pf_on()); break;
       case 0x10: case 0x11: case 0x12: case 0x13: case 0x14: {  // RESP0/1, RESM0/1, RESBL
         const int32_t hp = (int32_t)(T % 228u) - 68;
         const uint32_t base = r <= 0x11u ? 5u : 4u;
@@ -112,21 +107,25 @@ struct TiaP {
         if (r == 0x14u) w7 = with_byte(w7, 0, p);
         else w6 = with_byte(w6, (int)(r - 0x10u), p);
       } break;
-      case 0x1B: w2 = with_byte(w2, 2, v); w3 = with_byte(w3, 1, byte_of(w3, 0)); break;  // GRP0; GRP1 old <- new
+      case 0x1B:  // GRP0; GRP1 old <- new
+        w2 = with_byte(w2, 2, v); w3 = with_byte(w3, 1, byte_of(w3, 0));
+        set_pres(0, p0_on()); set_pres(1, p1_on());
+        break;
       case 0x1C:  // GRP1; GRP0 old <- new; ENABL old <- new
         w3 = with_byte(w3, 0, v);
         w2 = with_byte(w2, 3, byte_of(w2, 2));
         setf(6, f(5));
+        set_pres(0, p0_on()); set_pres(1, p1_on()); set_pres(4, ball_on());
         break;
-      case 0x1D: setf(3, v >> 1); break;
-      case 0x1E: setf(4, v >> 1); break;
-      case 0x1F: setf(5, v >> 1); break;
+      case 0x1D: setf(3, v >> 1); set_pres(2, m0_on()); break;
+      case 0x1E: setf(4, v >> 1); set_pres(3, m1_on()); break;
+      case 0x1F: setf(5, v >> 1); set_pres(4, ball_on()); break;
       case 0x20: w3 = with_byte(w3, 2, v >> 4); break;
       case 0x21: w3 = with_byte(w3, 3, v >> 4); break;
       case 0x22: case 0x23: case 0x24: w4 = with_byte(w4, (int)(r - 0x22u), v >> 4); break;
-      case 0x25: setf(7, v); break;
-      case 0x26: setf(8, v); break;
-      case 0x27: setf(9, v); break;
+      case 0x25: setf(7, v); set_pres(0, p0_on()); break;
+      case 0x26: setf(8, v); set_pres(1, p1_on()); break;
+      case 0x27: setf(9, v); set_pres(4, ball_on()); break;
       case 0x28: case 0x29: {  // RESMP: the missile locks to its player's centre on release
         const int b = r == 0x28u ? 10 : 11;
         const uint32_t nv = (v >> 1) & 1u;
@@ -137,6 +136,7 @@ struct TiaP {
           w6 = with_byte(w6, r == 0x28u ? 2 : 3, (pp + c) % 160u);
         }
         setf(b, nv);
+        set_pres(2, m0_on()); set_pres(3, m1_on());
       } break;
       case 0x2A: {  // HMOVE
         auto mv = [](uint32_t p, uint32_t hm) -> uint32_t {
@@ -154,7 +154,6 @@ struct TiaP {
       case 0x2C: w7 &= 0xFFFFu; break;               // CXCLR
       default: break;
     }
-    if ((kPresenceRegs >> r) & 1ull) poss = 0xFFFFFFFFu;
   }
 };
 
