@@ -499,7 +499,10 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   uint32_t ev = SE_NONE;
   // idle-loop skip (exact): the last plain timer read (offset, cycles, cycles its value holds, end)
   uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
-  const uint32_t skip_mask = M->idle_skip ? 0xFFFFFFFFu : 0u;
+  const bool skip = M->idle_skip != 0u;
+  // the RIOT timer's parameters stay in registers (only RIOT writes, in the general path, change them)
+  int32_t tW = M->tW;
+  uint32_t tVS = M->tV | (M->tS << 8);
   auto setnz = [&](uint32_t x) { nz = x * 257u; };  // x <= 0xFF
   auto adc = [&](uint32_t m) {
     if (!D) {
@@ -605,20 +608,12 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             setnz(v);
             break;
           case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
-            const int32_t et = (int32_t)now - M->tW;
-            const uint32_t tV = M->tV, tS = M->tS;
+            const int32_t et = (int32_t)now - tW;
+            const uint32_t tV = tVS & 0xFFu, tS = tVS >> 8;
             const int32_t VI = (int32_t)(tV << tS);
-            uint32_t ff = 0u;
-            if (hi & 1u) {  // TIMINT
-              v = et > VI ? 0x80u : 0u;
-              ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
-            } else if (et <= VI) {
-              const int32_t q = (et + (1 << tS) - 1) >> tS;
-              v = (tV - (uint32_t)q) & 0xFFu;
-              ff = (uint32_t)((q << tS) - et);
-            } else {
-              v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
-            }
+            if (hi & 1u) v = et > VI ? 0x80u : 0u;  // TIMINT
+            else if (et <= VI) v = (tV - (uint32_t)((et + (1 << tS) - 1) >> tS)) & 0xFFu;
+            else v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
             if (cls == C_TLD) {
               A = (aux & 1u) ? v : A;
               X = (aux & 2u) ? v : X;
@@ -627,10 +622,15 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             } else {
               nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u;
             }
-            pff = ff & skip_mask;
-            ppc = pco;
-            pn = now - fc;
-            pfe = now;
+            if (skip) {  // cycles over which the value read stays the same
+              uint32_t ff = 0u;
+              if (hi & 1u) ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
+              else if (et <= VI) ff = (uint32_t)((((et + (1 << tS) - 1) >> tS) << tS) - et);
+              pff = ff;
+              ppc = pco;
+              pn = now - fc;
+              pfe = now;
+            }
           } break;
           case C_STTIA: {
             const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
@@ -737,6 +737,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       nz = (M->zreg & 0xFFu) | ((M->nreg & 0x80u) << 8);
       fc = M->fc; bank = M->bank; log_len = M->log_len;
       ws_fc = fc; ws_now = M->t_phaseA / 3u;
+      tW = M->tW; tVS = M->tV | (M->tS << 8);
       if (kDebug && (r & kGenCommitted)) --budget;
       ev = r & 0xFFu;
       if (ev != SE_NONE) goto out;
