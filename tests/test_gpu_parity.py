@@ -371,3 +371,20 @@ def test_frame_stack_parity(roms):
         n_done += int(d2.sum())
     assert_same_state(gpu.get_state(), ref.get_state(), "end")
     assert n_done >= n
+
+
+@pytest.mark.parametrize("src", ["R1", "R2", "R4", "m20", "m21"])
+def test_idle_skip_is_exact(src):
+    """The exact idle-loop skip (cule_config.idle_skip; R#24) skips
+    whole [timer read; branch back] poll iterations in closed form: observations, rewards,
+    dones, counters and the full state stay bit-identical to the oracle, which never skips."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    rom = games.build_rom(src) if src.startswith("R") else micro.build(
+        micro.m20_timer_polls() if src == "m20" else micro.m21_timint_spin(100))
+    roms = [rom, games.build_rom("R1")]
+    n = 40
+    gpu = Env(roms, n, 4, reset_cache_size=4, idle_skip=1)
+    check_engine(gpu)
+    ref = oracle.OracleEnv(roms, n, 4, H.palette_rgb(), reset_cache_size=4)
+    run_parity(gpu, ref, 30, seed=77)
