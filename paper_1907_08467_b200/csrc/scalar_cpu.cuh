@@ -481,7 +481,9 @@ out:
 // only with PC in a cartridge window).  Phase A of an instruction samples at the end of the
 // previous one: that is fc, except right after a WSYNC stall, recorded as (ws_fc, ws_now) — fc
 // strictly increases within a call, so fc == ws_fc identifies the instruction after the stall.
-template <bool kDebug>
+// kSkip: the exact idle-loop skip is enabled (cule_config.idle_skip); compiled separately so
+// the headline path (skip off) carries none of its bookkeeping.
+template <bool kDebug, bool kSkip>
 __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_t dtab0, uint32_t ram0, uint32_t lg0,
                                             uint32_t log_lim, uint32_t cap_cycles, int32_t& budget,
                                             uint32_t rec_all0) {
@@ -499,7 +501,6 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   uint32_t ev = SE_NONE;
   // idle-loop skip (exact): the last plain timer read (offset, cycles, cycles its value holds, end)
   uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
-  const bool skip = M->idle_skip != 0u;
   // the RIOT timer's parameters stay in registers (only RIOT writes, in the general path, change them)
   int32_t tW = M->tW;
   uint32_t tVS = M->tV | (M->tS << 8);
@@ -564,7 +565,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           // in the same constant interval repeat this one exactly, so only time advances
           // (stopping short of the runaway cap, which the loop then reaches normally).
           // pfe == fc: the read was the instruction right before this branch.
-          if (!kDebug && pff != 0u && pfe == fc && npco == ppc && now < cap_cycles) {
+          if (kSkip && pff != 0u && pfe == fc && npco == ppc && now < cap_cycles) {
             const uint32_t P = pn + (now - fc);
             const uint32_t j = min(pff / P, (cap_cycles - 1u - now) / P);
             now += j * P;
@@ -622,7 +623,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             } else {
               nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u;
             }
-            if (skip) {  // cycles over which the value read stays the same
+            if (kSkip) {  // cycles over which the value read stays the same
               uint32_t ff = 0u;
               if (hi & 1u) ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
               else if (et <= VI) ff = (uint32_t)((((et + (1 << tS) - 1) >> tS) << tS) - et);

@@ -165,7 +165,11 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
                  lg_s = smem_addr(lg);
   for (;;) {
     uint32_t ev = SE_NONE;
-    if (lane == 0u) ev = run_cpu<kDebug>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget, rec_s);
+    if (lane == 0u) {
+      ev = (!kDebug && M->idle_skip)
+               ? run_cpu<kDebug, !kDebug>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget, rec_s)
+               : run_cpu<kDebug, false>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget, rec_s);
+    }
     ev = __shfl_sync(kFull, ev, 0);
     __syncwarp();
     const uint32_t n = M->log_len;
