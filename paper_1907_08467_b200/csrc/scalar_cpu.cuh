@@ -503,7 +503,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
   uint32_t ppc = 0xFFFFFFFFu, pn = 0u, pff = 0u, pfe = 0xFFFFFFFFu;
   // the RIOT timer's parameters stay in registers (only RIOT writes, in the general path, change them)
   int32_t tW = M->tW;
-  uint32_t tVS = M->tV | (M->tS << 8);
+  uint32_t tVS = M->tV | (M->tS << 8) | (((1u << M->tS) - 1u) << 16);  // V | shift << 8 | (2^shift - 1) << 16
   auto setnz = [&](uint32_t x) { nz = x * 257u; };  // x <= 0xFF
   auto adc = [&](uint32_t m) {
     if (!D) {
@@ -585,9 +585,10 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
         // data operand: RAM[(opnd + ix) & 0x7F] (needs bit 7 of opnd + ix, else the general
         // path: zp,X into the TIA) or the cartridge byte (opnd + ix) & 0xFFF of the bank
         const uint32_t opnd = hi >> pd::OPND;
-        const uint32_t t = opnd + prmt(X + Y * 256u, 0u, hi);
+        auto ea_t = [&]() { return opnd + prmt(X + Y * 256u, 0u, hi); };  // computed per case
         uint32_t v = 0u;
         auto rd_operand = [&]() -> bool {
+          const uint32_t t = ea_t();
           if (hi & pd::RAM) {
             if (!(t & 0x80u)) return false;
             v = ld_ram(ram0 + (t & 0x7Fu));
@@ -603,6 +604,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
           case C_LD:
             if (!rd_operand()) goto general;
+          ld_v:
             A = (aux & 1u) ? v : A;
             X = (aux & 2u) ? v : X;
             Y = (aux & 4u) ? v : Y;
@@ -610,28 +612,23 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             break;
           case C_TLD: case C_TBIT: {  // RIOT timer, closed form (R#24); an idle-loop head candidate
             const int32_t et = (int32_t)now - tW;
-            const uint32_t tV = tVS & 0xFFu, tS = tVS >> 8;
+            const uint32_t tV = tVS & 0xFFu, tS = (tVS >> 8) & 0xFFu, tm = tVS >> 16;  // tm = 2^tS - 1
             const int32_t VI = (int32_t)(tV << tS);
             if (hi & 1u) v = et > VI ? 0x80u : 0u;  // TIMINT
-            else if (et <= VI) v = (tV - (uint32_t)((et + (1 << tS) - 1) >> tS)) & 0xFFu;
+            else if (et <= VI) v = (tV - (uint32_t)((et + (int32_t)tm) >> tS)) & 0xFFu;
             else v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
-            if (cls == C_TLD) {
-              A = (aux & 1u) ? v : A;
-              X = (aux & 2u) ? v : X;
-              Y = (aux & 4u) ? v : Y;
-              setnz(v);
-            } else {
-              nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u;
-            }
             if (kSkip) {  // cycles over which the value read stays the same
               uint32_t ff = 0u;
               if (hi & 1u) ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
-              else if (et <= VI) ff = (uint32_t)((((et + (1 << tS) - 1) >> tS) << tS) - et);
+              else if (et <= VI) ff = (uint32_t)((((et + (int32_t)tm) >> tS) << tS) - et);
               pff = ff;
               ppc = pco;
               pn = now - fc;
               pfe = now;
             }
+            if (cls == C_TLD) goto ld_v;
+            nz = (A & v) | ((v & 0x80u) << 8);  // C_TBIT
+            V = (v >> 6) & 1u;
           } break;
           case C_STTIA: {
             const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
@@ -677,11 +674,13 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           case C_ADC: if (!rd_operand()) goto general; adc(v); break;
           case C_BIT: if (!rd_operand()) goto general; nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
           case C_NOPR: if (!rd_operand()) goto general; break;
-          case C_STRAM:
+          case C_STRAM: {
+            const uint32_t t = ea_t();
             if (!(t & 0x80u)) goto general;
             st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
-            break;
+          } break;
           case C_INC: case C_DEC: case C_ASL: case C_LSR: case C_ROL: case C_ROR: {
+            const uint32_t t = ea_t();
             if (!(t & 0x80u)) goto general;
             const uint32_t a = ram0 + (t & 0x7Fu);
             const uint32_t m = ld_ram(a);
@@ -738,7 +737,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
       nz = (M->zreg & 0xFFu) | ((M->nreg & 0x80u) << 8);
       fc = M->fc; bank = M->bank; log_len = M->log_len;
       ws_fc = fc; ws_now = M->t_phaseA / 3u;
-      tW = M->tW; tVS = M->tV | (M->tS << 8);
+      tW = M->tW; tVS = M->tV | (M->tS << 8) | (((1u << M->tS) - 1u) << 16);
       if (kDebug && (r & kGenCommitted)) --budget;
       ev = r & 0xFFu;
       if (ev != SE_NONE) goto out;
