@@ -173,9 +173,9 @@ static int choose_engine(int N) {
     if (!strcmp(v, "simt")) return 0;
     if (!strcmp(v, "scalar")) return 1;
   }
-  // measured (profiles/r01_v6_engine_sweep.txt): 4096 envs scalar 2.28M vs SIMT 0.75M FPS;
-  // 16384 (F8) 2.27M vs 2.31M; 32768 (4 ROMs) 1.80M vs 2.85M
-  return N <= 12288 ? 1 : 0;
+  // measured (profiles/r01_v6_engine_sweep.txt): 4096 envs scalar 2.70M vs SIMT 0.73M FPS;
+  // 16384 (F8) 2.65M vs 2.27M; 32768 (4 ROMs) 2.06M vs 2.77M
+  return N <= 16384 ? 1 : 0;
 }
 
 // Envs per warp: the per-env 6502 chain is latency-bound, so at low env counts the kernel
