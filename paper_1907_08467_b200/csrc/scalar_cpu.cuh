@@ -553,6 +553,9 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
     {
       uint32_t lo, hi;
       asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(recb + 8u * pco));
+      // back to the instruction's start for the general path: nothing was committed, and
+      // pco / fc are recovered from the record, so they need not stay live across the switch
+#define CULE_FALLBACK() do { pco = (lo >> pd::NXT) - ((lo >> pd::LENF) & 3u); fc = now - ((lo >> pd::CYC) & 0xFu); goto general; } while (0)
       const uint32_t cls = lo & 31u;
       uint32_t now = fc + ((lo >> pd::CYC) & 0xFu);
       uint32_t npco = lo >> pd::NXT;
@@ -576,7 +579,7 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           // after every instruction
           if (!kDebug && now >= cap_cycles) { pco = npco; fc = now; M->fault = 2u; ev = SE_FAULT; break; }
         } else {
-          now = fc + 2u;
+          now -= ((lo >> pd::CYC) & 0xFu) - 2u;  // not taken: 2 cycles
         }
         goto fast_done;
       }
@@ -600,10 +603,10 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
         };
         if (cls <= C_HOT_LAST) {
           switch (cls) {
-          case C_SBC: if (!rd_operand()) goto general; sbc(v); break;
-          case C_CMP: if (!rd_operand()) goto general; cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
+          case C_SBC: if (!rd_operand()) CULE_FALLBACK(); sbc(v); break;
+          case C_CMP: if (!rd_operand()) CULE_FALLBACK(); cmp(aux == 0u ? A : (aux == 1u ? X : Y), v); break;
           case C_LD:
-            if (!rd_operand()) goto general;
+            if (!rd_operand()) CULE_FALLBACK();
           ld_v:
             A = (aux & 1u) ? v : A;
             X = (aux & 2u) ? v : X;
@@ -664,24 +667,24 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             D = f == 2u ? b : D;
             V = f == 3u ? b : V;
           } break;
-          default: goto general;
+          default: CULE_FALLBACK();
           }
         } else {
           switch (cls) {
-          case C_ORA: if (!rd_operand()) goto general; A |= v; setnz(A); break;
-          case C_AND: if (!rd_operand()) goto general; A &= v; setnz(A); break;
-          case C_EOR: if (!rd_operand()) goto general; A ^= v; setnz(A); break;
-          case C_ADC: if (!rd_operand()) goto general; adc(v); break;
-          case C_BIT: if (!rd_operand()) goto general; nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
-          case C_NOPR: if (!rd_operand()) goto general; break;
+          case C_ORA: if (!rd_operand()) CULE_FALLBACK(); A |= v; setnz(A); break;
+          case C_AND: if (!rd_operand()) CULE_FALLBACK(); A &= v; setnz(A); break;
+          case C_EOR: if (!rd_operand()) CULE_FALLBACK(); A ^= v; setnz(A); break;
+          case C_ADC: if (!rd_operand()) CULE_FALLBACK(); adc(v); break;
+          case C_BIT: if (!rd_operand()) CULE_FALLBACK(); nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
+          case C_NOPR: if (!rd_operand()) CULE_FALLBACK(); break;
           case C_STRAM: {
             const uint32_t t = ea_t();
-            if (!(t & 0x80u)) goto general;
+            if (!(t & 0x80u)) CULE_FALLBACK();
             st_ram(ram0 + (t & 0x7Fu), aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
           } break;
           case C_INC: case C_DEC: case C_ASL: case C_LSR: case C_ROL: case C_ROR: {
             const uint32_t t = ea_t();
-            if (!(t & 0x80u)) goto general;
+            if (!(t & 0x80u)) CULE_FALLBACK();
             const uint32_t a = ram0 + (t & 0x7Fu);
             const uint32_t m = ld_ram(a);
             uint32_t r;
@@ -710,10 +713,11 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             npco = hi & 0xFFFu;
             if (!kDebug && now >= cap_cycles) { pco = npco; fc = now; M->fault = 2u; ev = SE_FAULT; goto out; }
             break;
-          default: goto general;
+          default: CULE_FALLBACK();
           }
         }
       }
+#undef CULE_FALLBACK
     fast_done:
       pco = npco;
       fc = now;

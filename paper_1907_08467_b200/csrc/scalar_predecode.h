@@ -25,8 +25,10 @@ namespace cule {
 
 namespace pd {
 // Record word lo: [0:5) class, [5:8) aux, [8:12) base cycles (C_BR: cycles when taken),
-// [20:32) low 12 bits of the fall-through PC (the instruction ends inside the 4 KB window).
-constexpr uint32_t AUX = 5, CYC = 8, NXT = 20;
+// [12:14) length, [20:32) low 12 bits of the fall-through PC (the instruction ends inside the
+// 4 KB window).  A class-0 (general path) record has cycles 0, length 0 and its own offset in
+// the NXT field, so the fast loop recovers PC and cycle of any record as nxt - len, now - cyc.
+constexpr uint32_t AUX = 5, CYC = 8, LENF = 12, NXT = 20;
 // Record word hi, by class:
 //   reads / stores / read-modify-writes: [0:16) byte-permute selector of the index (sk::SEL_*;
 //     bit 8 = page-cross penalty, which turns selector nibble 2 from 4 into 5: both pick a zero
@@ -182,7 +184,8 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
       default: break;
     }
   }
-  const uint32_t lo = cls | (raux << pd::AUX) | (cyc << pd::CYC) | (((o + len) & 0xFFFu) << pd::NXT);
+  const uint32_t lo = cls == C_GEN ? (o << pd::NXT)
+                                   : cls | (raux << pd::AUX) | (cyc << pd::CYC) | (len << pd::LENF) | ((o + len) << pd::NXT);
   return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
