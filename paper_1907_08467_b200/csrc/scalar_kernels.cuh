@@ -19,11 +19,11 @@
 namespace cule {
 
 // per-warp shared memory: [RAM 128][TIA words 48][SMach 128][state staging 80][log 4*kSLogCap]
-// [fused-observation ring 3 x 160]
+// [fused-observation ring 3 x 160][shaded colours 16]
 constexpr uint32_t kSLogCap = 128;
 constexpr uint32_t kSOffTia = 128, kSOffMach = 176, kSOffStg = 304, kSOffLog = 384;
 constexpr uint32_t kSOffRing = kSOffLog + 4 * kSLogCap;
-constexpr uint32_t kSWarpBytes = kSOffRing + 480;
+constexpr uint32_t kSWarpBytes = kSOffRing + 480 + 16;  // ring, shaded colour cache
 constexpr uint32_t kSWarps = CULE_SWARPS;  // warps per block (each warp emulates one env at a time)
 constexpr uint32_t kSmSDecode = kSmRom;  // scalar decode table [256] u64 right after the gray LUT
 constexpr uint32_t kSDecBytes = 2048;
@@ -147,6 +147,8 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
   rb.prev = (kGray && nframes >= 2u) ? frame_out : nullptr;  // frame fs-1, staged by this step
   rb.ring_s = smem_addr(ring);
   rb.cols_s = smem_addr(cols);
+  shade_init(rb.ring_s + kShadeOff, tw[0], gray);  // colours as loaded (all lanes, same values)
+  __syncwarp();
   rb.r0 = rb.r1 = rb.r2 = rb.r3 = fill;
   uint32_t f = 0;
   int32_t status = RUN_FRAME;

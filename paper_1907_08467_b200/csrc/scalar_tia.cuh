@@ -242,6 +242,16 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
   return v;
 }
 
+// shaded colour cache: 4 words (COLUP0, COLUP1, COLUPF, COLUBK) right after the warp's ring;
+// every lane writes the same word, so each lane's later reads see it without a barrier
+constexpr uint32_t kShadeOff = 480;
+__device__ __forceinline__ void shade_store(uint32_t a, uint32_t colu, const uint8_t* gray) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(Tia::shade(colu, gray)) : "memory");
+}
+__device__ __forceinline__ void shade_init(uint32_t shade_s, uint32_t w0, const uint8_t* gray) {
+  for (uint32_t k = 0; k < 4; ++k) shade_store(shade_s + 4u * k, (w0 >> (8 * k)) & 0xFFu, gray);
+}
+
 // output row i (0..83) of the exact area average from input rows r0, r0+1, r0+2 of the ring
 // (rows weighted 2:2:1 for even i, 1:2:2 for odd i; total weight 200, round half to even, R#17)
 __device__ __forceinline__ void area84_row(uint32_t ring_s, uint32_t cols_s, uint32_t r0, uint32_t i, uint8_t* out,
@@ -311,10 +321,11 @@ __device__ __forceinline__ uint32_t collide_coop(const Words& w, uint32_t lane, 
 }
 
 // the 16 pixels of the lane's chunk (4 words of 4 bytes) with the registers of the current span
-__device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t lane, const uint8_t* gray,
+__device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t lane, uint32_t shade_s,
                                          uint32_t& x0w, uint32_t& x1w, uint32_t& x2w, uint32_t& x3w) {
-  const uint32_t cbk = Tia::shade(byte_of(t.w0, 3), gray), c0 = Tia::shade(byte_of(t.w0, 0), gray),
-                 c1 = Tia::shade(byte_of(t.w0, 1), gray), cbl = Tia::shade(byte_of(t.w0, 2), gray);
+  // the four shaded colour words (COLUP0, COLUP1, COLUPF, COLUBK), kept current by flush_coop
+  uint32_t c0, c1, cbl, cbk;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(c0), "=r"(c1), "=r"(cbl), "=r"(cbk) : "r"(shade_s) : "memory");
   const uint32_t ctrlpf = byte_of(t.w1, 3);
   const uint32_t cp = (ctrlpf & 2u) ? (lane < 5u ? c0 : c1) : cbl;  // score mode: P0/P1 colour per half
   const uint32_t hs = 16u * (lane & 1u);
@@ -381,7 +392,7 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   }
   if (!any_win) return;
   uint32_t x0w = rb.fill, x1w = rb.fill, x2w = rb.fill, x3w = rb.fill;
-  if (!vblank && lane < 10u) chunk_px(t, w, lane, gray, x0w, x1w, x2w, x3w);
+  if (!vblank && lane < 10u) chunk_px(t, w, lane, rb.ring_s + kShadeOff, x0w, x1w, x2w, x3w);
   const int32_t comb = vblank ? -1 : t.comb_line();
   const uint32_t la = l0 > w0 ? l0 : w0, lb = l1 < w1 - 1u ? l1 : w1 - 1u;
   const uint32_t cx = 16u * lane;
@@ -417,6 +428,7 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
     catch_up_coop(t, T, rb, lane, ystart, gray, w, dirty);
     __syncwarp();  // reconverge: the register update is warp-uniform work, issued once
     t.apply(r, e & 0xFFu, T);
+    if (r - 6u < 4u) shade_store(rb.ring_s + kShadeOff + 4u * (r - 6u), e & 0xFFu, gray);  // COLUxx
     dirty |= kDirtyTable.v[r];
   }
   if (fin) catch_up_coop(t, t_final, rb, lane, ystart, gray, w, dirty);
