@@ -31,6 +31,10 @@ CONFIGS = {
     "cfg2": (["R1"], 4096, 4, "gray84", "cfg2: 4096 envs, generated 4 KB ROM R1, fs=4, GRAY84"),
     "cfg3": (["R2"], 16384, 4, "gray84", "cfg3: 16384 envs, F8 ROM R2, fs=4, GRAY84, reset-from-cache"),
     "cfg4": (["R1", "R2", "R3", "R4"], 32768, 4, "gray84", "cfg4: 32768 envs, R1-R4 interleaved, fs=4, GRAY84"),
+    # cfg5 is the whole-box configuration: 262144 envs = 32768 per GPU over 8 GPUs (run it with
+    # torchrun --nproc-per-node 8 ... --config cfg5); per GPU it is the cfg4 workload
+    "cfg5": (["R1", "R2", "R3", "R4"], 32768, 4, "gray84",
+             "cfg5: 32768 envs per GPU (262144 on 8 GPUs), R1-R4 interleaved, fs=4, GRAY84"),
     # analysis variants (not bench lines): cfg2 with RAW observations (1 of 4 frames rendered)
     "cfg2raw": (["R1"], 4096, 4, "raw", "cfg2raw: 4096 envs, generated 4 KB ROM R1, fs=4, RAW frames"),
 }
