@@ -356,10 +356,17 @@ static uint8_t timer_timint(const Machine* m) {
 /* ------------------------------------------------------------------------------------------ */
 /* Bus (§8(c).3, cartridge §8(c).6)                                                           */
 /* ------------------------------------------------------------------------------------------ */
+/* Bank switching (Atari standard schemes; SURVEY.md §8(f) NEXT-4 widens the paper's 4K/F8):
+ * F8 (8 KB, 2 banks): an access to $1FF8 / $1FF9 selects bank 0 / 1;
+ * F6 (16 KB, 4 banks): $1FF6 .. $1FF9 select banks 0 .. 3;
+ * F4 (32 KB, 8 banks): $1FF4 .. $1FFB select banks 0 .. 7.
+ * 2K and 4K cartridges have no hotspots. */
 static void cart_hotspot(Machine* m, uint16_t a) {
-  if (m->rom_len == 8192) {
-    if (a == 0x1FF8) m->bank = 0;
-    if (a == 0x1FF9) m->bank = 1;
+  switch (m->rom_len) {
+    case 8192: if (a >= 0x1FF8 && a <= 0x1FF9) m->bank = (uint8_t)(a - 0x1FF8); break;
+    case 16384: if (a >= 0x1FF6 && a <= 0x1FF9) m->bank = (uint8_t)(a - 0x1FF6); break;
+    case 32768: if (a >= 0x1FF4 && a <= 0x1FFB) m->bank = (uint8_t)(a - 0x1FF4); break;
+    default: break;
   }
 }
 
@@ -367,6 +374,7 @@ static uint8_t rd(Machine* m, uint16_t addr) {
   uint16_t a = addr & 0x1FFF;
   if (a & 0x1000) {
     cart_hotspot(m, a);
+    if (m->rom_len == 2048) return m->rom[a & 0x07FF]; /* 2K: mirrored twice in the window */
     return m->rom[(size_t)m->bank * 4096 + (a & 0x0FFF)];
   }
   if (!(a & 0x0080)) return tia_read(m, a & 0x0F);
@@ -825,7 +833,7 @@ static void power_on(Machine* m, const uint8_t* rom, size_t rom_len) {
   bind(m, rom, rom_len);
   m->SP = 0xFD;
   m->P = 0x24;
-  m->bank = (uint8_t)(rom_len / 4096 - 1); /* last bank [R#23] */
+  m->bank = (uint8_t)(rom_len > 4096 ? rom_len / 4096 - 1 : 0); /* last bank [R#23] */
   m->timer_s = 10;
   m->timer_v = 0;
   m->timer_w = 0;
@@ -869,7 +877,7 @@ static void latch_inputs(Machine* m, int action) {
   m->inpt4 = fire ? 0x00 : 0x80;
 }
 
-static int valid_rom_len(size_t n) { return n == 4096 || n == 8192; }
+static int valid_rom_len(size_t n) { return n == 2048 || n == 4096 || n == 8192 || n == 16384 || n == 32768; }
 
 /* ------------------------------------------------------------------------------------------ */
 /* machine-level C-ABI                                                                         */

@@ -88,13 +88,14 @@ class AsmError(Exception):
 
 
 class Assembler:
-    """Assemble source text into a ROM image of `size` bytes (4096 or 8192)."""
+    """Assemble source text into a ROM image of `size` bytes: 2048 (2K, mirrored in the 4 KB
+    window), 4096, or 4096 x banks (8192 F8, 16384 F6, 32768 F4; `.bank N` selects the bank)."""
 
     def __init__(self, size: int = 4096):
-        if size not in (4096, 8192):
-            raise AsmError("ROM size must be 4096 or 8192")
+        if size not in (2048, 4096, 8192, 16384, 32768):
+            raise AsmError("ROM size must be 2048, 4096, 8192, 16384 or 32768")
         self.size = size
-        self.nbanks = size // 4096
+        self.nbanks = max(1, size // 4096)
 
     # -- expressions -------------------------------------------------------------------
     def _eval(self, expr: str, syms: dict[str, int], strict: bool) -> int | None:
@@ -340,7 +341,7 @@ class Assembler:
             a = pc + i
             if not 0xF000 <= a <= 0xFFFF:
                 raise AsmError(f"address ${a:04X} outside the $F000-$FFFF cartridge window")
-            image[bank * 4096 + (a & 0xFFF)] = b
+            image[(a & 0x7FF) if self.size == 2048 else bank * 4096 + (a & 0xFFF)] = b
 
 
 def assemble(source: str, size: int = 4096) -> bytes:

@@ -667,3 +667,62 @@ L2: STA WSYNC
     BNE L2
     JMP Frame
 """ + _VECTORS
+
+
+# ---------------------------------------------------------------------------------------------
+# M22 bank-switching schemes beyond F8 (SURVEY.md §8(f) NEXT-4): F6 (4 banks, $1FF6-$1FF9)
+# and F4 (8 banks, $1FF4-$1FFB), plus the mirrored 2K cartridge
+# ---------------------------------------------------------------------------------------------
+def m22_banks(nbanks: int) -> str:
+    """Power-on runs the last bank.  Bank b stores $B0+b at RAM $80+b and switches to bank b-1
+    through `LDA HS,X` (X = b-1) in a stub that sits at the same address in every bank; the
+    stub's next instruction runs in the new bank and stores the byte the hotspot read returned
+    (the new bank's marker 16*(b-1) + (b-1)) at RAM $90+X.  Bank 0 ends in a loop."""
+    hs = {4: 0x1FF6, 8: 0x1FF4}[nbanks]
+    src = [EQUATES]
+    for b in range(nbanks):
+        body = [f".bank {b}", "    .org $F000", f"Entry{b}:", "    SEI", "    CLD", "    LDX #$FF", "    TXS",
+                f"    LDA #${0xB0 + b:02X}", f"    STA ${0x80 + b:02X}"]
+        if b == 0:
+            body += ["Done:", "    JMP Done"]
+        else:
+            body += [f"    LDX #{b - 1}", "    JMP $FF00"]
+        body += ["    .org $FF00", f"    LDA ${hs:04X},X", "    STA $90,X", "    JMP $F000",
+                 f"    .org ${0xF000 | (hs & 0xFFF):04X}",
+                 "    .byte " + ", ".join(f"${16 * b + k:02X}" for k in range(nbanks)),
+                 "    .org $FFFC", f"    .word Entry{b}", f"    .word Entry{b}"]
+        src.append("\n".join(body))
+    return "\n".join(src) + "\n"
+
+
+def m22_2k() -> str:
+    """A 2 KB cartridge answers at $1000-$17FF and again at $1800-$1FFF: the program runs at
+    $F800, jumps into the mirror at $F000 + (same offset) and reads a table through both
+    mirrors.  RAM $80 counts passes (2), $81/$82 hold the table byte read through $F7xx/$FFxx."""
+    return EQUATES + """
+    .org $F800
+Reset:
+    SEI
+    CLD
+    LDX #$FF
+    TXS
+    LDA #0
+    STA $80
+Pass:
+    INC $80
+    LDA $80
+    CMP #2
+    BCS Both
+    JMP Pass - $800
+Both:
+    LDA Tab - $800
+    STA $81
+    LDA Tab
+    STA $82
+Done:
+    JMP Done
+Tab: .byte $5A
+    .org $FFFC
+    .word Reset
+    .word Reset
+"""

@@ -65,6 +65,29 @@ def test_m11_f8_bank_switching(orc):
     assert s[H.OFF["bank"]] == 1
 
 
+@pytest.mark.parametrize("nbanks", [4, 8])
+def test_m22_f6_f4_bank_switching(orc, nbanks):
+    # F6 ($1FF6-$1FF9) and F4 ($1FF4-$1FFB): power-on in the last bank; every bank stores its
+    # id; an indexed read of hotspot X switches to bank X first and returns that bank's marker
+    rom = micro.build(micro.m22_banks(nbanks), 4096 * nbanks)
+    s = orc.power_on(rom)
+    assert s[H.OFF["bank"]] == nbanks - 1 and H.pc(s) == 0xF000
+    orc.exec_instr(rom, s, 400)
+    assert [H.ram(s, 0x80 + b) for b in range(nbanks)] == [0xB0 + b for b in range(nbanks)]
+    assert [H.ram(s, 0x90 + x) for x in range(nbanks - 1)] == [17 * x for x in range(nbanks - 1)]
+    assert s[H.OFF["bank"]] == 0
+
+
+def test_m22_2k_mirror(orc):
+    # a 2 KB cartridge repeats at $1000-$17FF and $1800-$1FFF: code and data through both
+    rom = micro.build(micro.m22_2k(), 2048)
+    assert len(rom) == 2048
+    s = orc.power_on(rom)
+    assert s[H.OFF["bank"]] == 0 and H.pc(s) == 0xF800
+    orc.exec_instr(rom, s, 100)
+    assert [H.ram(s, a) for a in (0x80, 0x81, 0x82)] == [2, 0x5A, 0x5A]
+
+
 def test_m13_jmp_indirect_page_bug(orc):
     rom = micro.build(micro.m13_jmp_ind())
     s = run_until_done(orc, rom, 50)
