@@ -39,7 +39,8 @@ extern "C" {
 
 #define CULE_OK 0
 #define CULE_E_INVAL (-1)    /* bad argument (null pointer, size, range, workspace too small) */
-#define CULE_E_ROM_SIZE (-2) /* ROM length not in {4096 (4K), 8192 (F8)}           */
+#define CULE_E_ROM_SIZE (-2) /* ROM length not in {2048 (2K), 4096 (4K), 8192 (F8), 16384 (F6),
+                                32768 (F4)} (2K/F6/F4: SURVEY.md §8(f) NEXT-4) */
 #define CULE_E_ROM_FAULT (-3)/* the reset-cache build hit a JAM or a runaway frame             */
 #define CULE_E_CUDA (-4)     /* CUDA launch / runtime failure                                  */
 #define CULE_E_CLOSED (-5)   /* use after cule_destroy                             */
@@ -80,7 +81,11 @@ size_t cule_workspace_bytes(int num_envs, int n_roms, const cule_config* cfg);
 
 /* Create a batch of num_envs environments.  Env with global id g = env_index_base + i runs
  * ROM g % n_roms.  roms[r] / rom_lens[r] are HOST buffers (copied; may be freed afterwards);
- * 1 <= n_roms <= 4; each length must be 4096 (4K) or 8192 (F8).  d_workspace (device,
+ * 1 <= n_roms <= 4; each length must be 2048 (2K, mirrored in the 4 KB window), 4096 (4K),
+ * 8192 (F8: 2 banks, hotspots $1FF8-$1FF9), 16384 (F6: 4 banks, $1FF6-$1FF9) or 32768 (F4:
+ * 8 banks, $1FF4-$1FFB); any access to a hotspot switches bank (R#31, R#34).  The
+ * scalar engine needs its pre-decoded records (8 B per ROM byte) in shared memory: up to
+ * 20 KB of ROM in total; larger sets run on the batched engine.  d_workspace (device,
  * >= cule_workspace_bytes, 256-byte aligned) must outlive the handle.  Builds the reset cache
  * on the device (synchronous: returns after the build, CULE_E_ROM_FAULT if any entry faulted).
  * The handle uses the device current at the call.  Errors: CULE_E_INVAL, CULE_E_ROM_SIZE,

@@ -46,7 +46,7 @@ struct Ctx {
 struct Cpu {
   uint32_t PC, A, X, Y, SP, C, V, D, I, nreg, zreg;
   uint32_t fc, now, t_phaseA;
-  uint32_t bank, rom_off, is_f8, flim;
+  uint32_t bank, rom_off, hs_lo, nbank, flim;
   uint32_t tV, tS, swcha, inpt4;
   int32_t tW;
   uint32_t vsync, log_len, fault;
@@ -108,10 +108,10 @@ struct Cpu {
   __device__ __forceinline__ uint32_t rd(const Ctx& c, uint32_t addr) {
     const uint32_t a = addr & 0x1FFFu;
     const bool cart = (a & 0x1000u) != 0;
-    const bool hot = cart && is_f8 && ((a & 0x1FFEu) == 0x1FF8u);
+    const bool hot = cart && ((a & 0xFFFu) - hs_lo) < nbank;
     const bool ram = !cart && ((a & 0x0280u) == 0x0080u);
     if (cart | ram) {
-      if (hot) bank = a & 1u;
+      if (hot) bank = (a & 0xFFFu) - hs_lo;
       const uint32_t off = cart ? c.rom0 + rom_off + (bank << 12) + (a & 0xFFFu) : ram_addr(c, a & 0x7Fu);
       return c.smem[off];
     }
@@ -127,7 +127,7 @@ struct Cpu {
     const uint32_t a = addr & 0x1FFFu;
     if ((a & 0x1280u) == 0x0080u) { c.smem[ram_addr(c, a & 0x7Fu)] = (uint8_t)v; return; }
     if (a & 0x1000u) {
-      if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+      if (((a & 0xFFFu) - hs_lo) < nbank) bank = (a & 0xFFFu) - hs_lo;
       return;
     }
     if (!(a & 0x80u)) {

@@ -56,10 +56,10 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   L->cobs = take(nk * ob);
   L->cscore = take(2 * nk);
   L->cstage = take(gray ? 2 * nk * cule::kFrameBytes : 0);
-  L->roms = take(4 * 8192);
+  L->roms = take(4 * 32768);
   L->decode = take(2048);
   L->sdecode = take(2048);
-  L->srec = take(cule::kRecBytes * 4 * 8192);
+  L->srec = take(cule::kRecBytes * 4 * 32768);
   L->gray = take(128);
   L->counters = take(32);
   L->err = take(16);
@@ -81,7 +81,7 @@ struct cule_env {
   Layout L;
   uint32_t rom_off[4];
   uint32_t rom_bytes;
-  uint32_t f8_mask;
+  uint32_t rom_banks;      // 4 KB banks per ROM, 8 bits each (kernels.cuh banks_of)
   uint64_t pick_seed;
   size_t smem;
   uint32_t block;
@@ -103,7 +103,7 @@ static cule::Params base_params(const cule_env* e) {
   p.roms = e->ws + e->L.roms;
   p.rom_bytes = e->rom_bytes;
   for (int r = 0; r < 4; ++r) p.rom_off[r] = e->rom_off[r];
-  p.f8_mask = e->f8_mask;
+  p.rom_banks = e->rom_banks;
   p.n_roms = (uint32_t)e->n_roms;
   p.decode = reinterpret_cast<const uint64_t*>(e->ws + e->L.decode);
   p.sdecode = reinterpret_cast<const uint64_t*>(e->ws + e->L.sdecode);
@@ -254,8 +254,10 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   if (((uintptr_t)d_workspace & 255) != 0) return fail(CULE_E_INVAL, "workspace must be 256-byte aligned");
   for (int r = 0; r < n_roms; ++r) {
     if (!roms[r]) return fail(CULE_E_INVAL, "null ROM");
-    if (rom_lens[r] != 4096 && rom_lens[r] != 8192)
-      return fail(CULE_E_ROM_SIZE, "ROM size must be 4096 (4K) or 8192 (F8), got " + std::to_string(rom_lens[r]));
+    const size_t n = rom_lens[r];
+    if (n != 2048 && n != 4096 && n != 8192 && n != 16384 && n != 32768)
+      return fail(CULE_E_ROM_SIZE, "ROM size must be 2048 (2K), 4096 (4K), 8192 (F8), 16384 (F6) or 32768 (F4), got " +
+                                       std::to_string(n));
   }
   Layout L;
   compute_layout(num_envs, n_roms, cfg, &L);
@@ -272,13 +274,15 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   e->ws = static_cast<uint8_t*>(d_workspace);
   e->L = L;
   e->pick_seed = 0;
-  e->f8_mask = 0;
+  e->rom_banks = 0;
   uint32_t off = 0;
   for (int r = 0; r < 4; ++r) e->rom_off[r] = 0;
+  // images in 4 KB banks: a 2K cartridge is stored twice (its mirror in the 4 KB window)
   for (int r = 0; r < n_roms; ++r) {
     e->rom_off[r] = off;
-    off += (uint32_t)rom_lens[r];
-    if (rom_lens[r] == 8192) e->f8_mask |= 1u << r;
+    const uint32_t img = rom_lens[r] < 4096 ? 4096u : (uint32_t)rom_lens[r];
+    off += img;
+    e->rom_banks |= (img / 4096u) << (8 * r);
   }
   e->rom_bytes = off;
   e->epw = choose_epw(num_envs);
@@ -317,8 +321,12 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   const size_t smem_max = cule::smem_bytes(e->rom_bytes, kMaxBlock);
 
   // static inputs: ROM images, decode table, gray LUT (ITU-R 601 integer, half-up, §8(c).12)
-  uint8_t romimg[4 * 8192];
-  for (int r = 0; r < n_roms; ++r) std::memcpy(romimg + e->rom_off[r], roms[r], rom_lens[r]);
+  std::vector<uint8_t> romimg_v((size_t)e->rom_bytes);
+  uint8_t* romimg = romimg_v.data();
+  for (int r = 0; r < n_roms; ++r) {
+    std::memcpy(romimg + e->rom_off[r], roms[r], rom_lens[r]);
+    if (rom_lens[r] == 2048) std::memcpy(romimg + e->rom_off[r] + 2048, roms[r], 2048);  // 2K mirror
+  }
   uint64_t table[256];
   cule::build_decode_table(table);
   uint64_t stable[256];
@@ -326,7 +334,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   std::vector<uint64_t> recs((size_t)e->rom_bytes);
   {
     uint32_t lens[4] = {0, 0, 0, 0};
-    for (int r = 0; r < n_roms; ++r) lens[r] = (uint32_t)rom_lens[r];
+    for (int r = 0; r < n_roms; ++r) lens[r] = 4096u * cule::banks_of(e->rom_banks, (uint32_t)r);
     cule::predecode_roms(romimg, e->rom_off, lens, n_roms, recs.data());
   }
   uint8_t gray[128] = {0};

@@ -37,7 +37,7 @@ struct Params {
   const uint8_t* roms;       // packed ROM images (global)
   uint32_t rom_bytes;
   uint32_t rom_off[4];
-  uint32_t f8_mask;
+  uint32_t rom_banks;        // 4 KB banks per ROM, packed 8 bits per ROM: 1 (2K/4K), 2 (F8), 4 (F6), 8 (F4)
   uint32_t n_roms;
   const uint64_t* decode;    // [256] batched-engine decode table
   const uint64_t* sdecode;   // [256] scalar-engine decode table
@@ -73,6 +73,16 @@ struct Params {
   uint32_t obs_stride;
   uint32_t stacked, stack_slot;
 };
+
+// cartridge bank switching (F8 / F6 / F4; DESIGN.md §2 R#31, R#34): banks of ROM r, and the
+// window offset of its first hotspot ($FF8 / $FF6 / $FF4; 0x1000 = none).  An access to window
+// offset o switches to bank o - hs_lo when that is below the bank count.
+__host__ __device__ __forceinline__ uint32_t banks_of(uint32_t rom_banks, uint32_t r) {
+  return (rom_banks >> (8u * r)) & 0xFFu;
+}
+__host__ __device__ __forceinline__ uint32_t hs_lo_of(uint32_t banks) {
+  return banks == 2u ? 0xFF8u : (banks == 4u ? 0xFF6u : (banks == 8u ? 0xFF4u : 0x1000u));
+}
 
 // frame stack: all four slots of env i <- the cached start observation of entry ent
 __device__ __forceinline__ void stack_fill(const Params& p, uint32_t i, uint32_t ent, uint32_t lane) {
@@ -140,7 +150,7 @@ __device__ __forceinline__ Ctx stage_block(const Params& p, uint8_t* smem, bool 
     bulk_g2s(smem + kSmDecode, p.decode, 2048u, bar);
     bulk_g2s(smem + kSmGray, p.gray, 128u, bar);
     for (uint32_t r = 0; r < p.n_roms; ++r) {
-      uint32_t len = ((p.f8_mask >> r) & 1u) ? 8192u : 4096u;
+      const uint32_t len = 4096u * banks_of(p.rom_banks, r);
       bulk_g2s(smem + kSmRom + p.rom_off[r], p.roms + p.rom_off[r], len, bar);
     }
   }
@@ -186,8 +196,9 @@ __device__ __forceinline__ void load_machine(Cpu& m, const Ctx& c, const Hdr& h,
   m.vsync = hb(h, 24);
   const uint32_t rom_id = hb(h, 61);
   m.rom_off = p.rom_off[rom_id];
-  m.is_f8 = (p.f8_mask >> rom_id) & 1u;
-  m.flim = m.is_f8 ? 0xFF5u : 0xFFDu;
+  m.nbank = banks_of(p.rom_banks, rom_id);
+  m.hs_lo = hs_lo_of(m.nbank);
+  m.flim = m.nbank > 1u ? m.hs_lo - 3u : 0xFFDu;  // fast fetch: pc..pc+2 clear of the hotspots
   m.fault = hb(h, 62);
   m.log_len = 0;
   m.t_phaseA = 3u * m.fc;
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(128) cache_kernel(Params p) {
     Hdr h;
     for (int q = 0; q < 4; ++q) h.c[q] = make_uint4(0, 0, 0, 0);
     h.c[0].x = pk(0, 0, 0, 0xFD);
-    h.c[0].y = pk(0x24, (p.f8_mask >> r) & 1u, 0, 0);
+    h.c[0].y = pk(0x24, banks_of(p.rom_banks, r) - 1u, 0, 0);
     h.c[1].x = pk(0, 10, 0xFF, 0x80);
     h.c[1].y = 0xFFFF0000u;  // coll 0, comb_line -1
     h.c[3].w = pk(0, r, 0, 0);

@@ -35,7 +35,7 @@ struct SMach {
   uint32_t tV, tS, swcha, inpt4, vsync, fault;
   int32_t tW;
   uint32_t rom0;      // shared-memory offset of this env's ROM image
-  uint32_t is_f8;
+  uint32_t cart;      // bank switching: first hotspot window offset | banks << 16 (kernels.cuh hs_lo_of)
   uint32_t coll;      // collision latches at colour clock tia_done
   uint32_t tia_done;  // the TIA has been replayed to this colour clock
   uint32_t pa_T, pa_coll;  // latches kept for a phase-A read at pa_T (see run_cpu)
@@ -135,7 +135,7 @@ __device__ __noinline__ uint32_t s_fetch_slow(SMach* M, uint32_t rom0, uint32_t 
     const uint32_t a = (pc0 + k) & 0x1FFFu;
     uint32_t v;
     if (a & 0x1000u) {
-      if (M->is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+      if (((a & 0xFFFu) - (M->cart & 0xFFFFu)) < (M->cart >> 16)) bank = (a & 0xFFFu) - (M->cart & 0xFFFFu);
       v = ld_ro8(rom0 + (bank << 12) + (a & 0xFFFu));
     } else if ((a & 0x0280u) == 0x0080u) {
       v = ld_ram(ram0 + (a & 0x7Fu));
@@ -166,9 +166,9 @@ __device__ __noinline__ uint32_t s_gen_one(SMach* M, uint32_t rom_all0, uint32_t
   const uint32_t pend = M->t_phaseA / 3u;  // end cycle of the previous instruction
   uint32_t pnext = pend;
   const uint32_t rom0 = rom_all0 + M->rom0;
-  const uint32_t is_f8 = M->is_f8;
-  const uint32_t flim = is_f8 ? 0xFF5u : 0xFFDu;  // fast fetch: pc..pc+2 inside the page, no hotspot
-  const uint32_t hlim = is_f8 ? 0xFF7u : 0xFFFu;  // fast data read: no hotspot
+  const uint32_t hs_lo = M->cart & 0xFFFFu, nbank = M->cart >> 16;
+  const uint32_t flim = nbank > 1u ? hs_lo - 3u : 0xFFDu;  // fast fetch: pc..pc+2 inside the page, no hotspot
+  const uint32_t hlim = nbank > 1u ? hs_lo - 1u : 0xFFFu;  // fast data read: no hotspot
   uint32_t ev = SE_NONE, committed = 0u;
   auto nz = [&](uint32_t x) { nreg = x; zreg = x; };
   auto adc = [&](uint32_t m) {
@@ -226,7 +226,7 @@ __device__ __noinline__ uint32_t s_gen_one(SMach* M, uint32_t rom_all0, uint32_t
     auto rd = [&](uint32_t addr, uint32_t T, uint32_t pa) -> uint32_t {
       const uint32_t a = addr & 0x1FFFu;
       if (a & 0x1000u) {
-        if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+        if (((a & 0xFFFu) - hs_lo) < nbank) bank = (a & 0xFFFu) - hs_lo;
         return ld_ro8(rom0 + (bank << 12) + (a & 0xFFFu));
       }
       if ((a & 0x0280u) == 0x0080u) return ld_ram(ram0 + (a & 0x7Fu));
@@ -312,7 +312,7 @@ __device__ __noinline__ uint32_t s_gen_one(SMach* M, uint32_t rom_all0, uint32_t
             xf |= s_wr_slow(M, a, val, now);
           }
         } else if (a & 0x1000u) {
-          if (is_f8 && (a & 0x1FFEu) == 0x1FF8u) bank = a & 1u;
+          if (((a & 0xFFFu) - hs_lo) < nbank) bank = (a & 0xFFFu) - hs_lo;
         } else {
           s_wr_slow(M, a, val, now);  // RIOT
         }

@@ -58,7 +58,7 @@ __device__ __forceinline__ void load_smach(SMach* M, const Hdr& h, const Params&
   M->vsync = hb(h, 24);
   const uint32_t rom_id = hb(h, 61);
   M->rom0 = p.rom_off[rom_id];
-  M->is_f8 = (p.f8_mask >> rom_id) & 1u;
+  M->cart = hs_lo_of(banks_of(p.rom_banks, rom_id)) | (banks_of(p.rom_banks, rom_id) << 16);
   M->fault = hb(h, 62);
   M->log_len = 0u;
   M->t_phaseA = 3u * M->fc;
@@ -214,7 +214,7 @@ __device__ __forceinline__ void stage_block_s(const Params& p, uint8_t* smem) {
     bulk_g2s(smem + kSmGray, p.gray, 128u, bar);
     uint8_t* rec = smem + scalar_rec_off(p.rom_bytes);
     for (uint32_t r = 0; r < p.n_roms; ++r) {
-      const uint32_t len = ((p.f8_mask >> r) & 1u) ? 8192u : 4096u;
+      const uint32_t len = 4096u * banks_of(p.rom_banks, r);
       bulk_g2s(smem + kSmSDecode + kSDecBytes + p.rom_off[r], p.roms + p.rom_off[r], len, bar);
       if (p.use_rec) bulk_g2s(rec + kRecBytes * p.rom_off[r], p.srec + p.rom_off[r], kRecBytes * len, bar);
     }

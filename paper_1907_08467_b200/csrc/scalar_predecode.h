@@ -72,7 +72,11 @@ constexpr uint32_t C_HOT_LAST = C_WSYNC;
 constexpr uint32_t kRecBytes = 8;
 
 // decode the record for an instruction starting at bank offset o of a 4 KB bank image
-inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const uint64_t* stab) {
+inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, uint32_t nbanks, const uint64_t* stab) {
+  // hotspots of the bank-switching scheme: window offsets [hs, hs + nbanks) (F8 $FF8, F6 $FF6,
+  // F4 $FF4); none for one-bank cartridges
+  const uint32_t hs = nbanks == 2u ? 0xFF8u : (nbanks == 4u ? 0xFF6u : (nbanks == 8u ? 0xFF4u : 0x1000u));
+  auto hot = [&](uint32_t off) { return nbanks > 1u && off >= hs && off < hs + nbanks; };
   const uint32_t op = bank[o];
   const uint64_t ent = stab[op];
   const uint32_t d = (uint32_t)ent, e = (uint32_t)(ent >> 32);
@@ -86,9 +90,8 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
   const bool pen = (d & sk::PEN) != 0u;
   // the whole instruction must be fetched from this bank window without touching a hotspot
   bool fast = kind != K_JAM && o + len - 1 <= 0xFFFu;
-  if (f8)
-    for (uint32_t k = 0; k < len; ++k)
-      if (o + k == 0xFF8u || o + k == 0xFF9u) fast = false;
+  for (uint32_t k = 0; k < len; ++k)
+    if (hot(o + k)) fast = false;
   const bool zp = (d & sk::ZP) != 0u, ptr = (d & (sk::PTRZ | sk::PTRA)) != 0u;
   const bool imm = len == 2 && !zp && !ptr && kind != K_BR && !(d & sk::RD) && !(d & sk::WR);
   const bool indexed = sel != sk::SEL_NONE;
@@ -103,7 +106,7 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
     const uint32_t a = base & 0x1FFFu;
     if (!indexed) {
       if ((a & 0x1280u) == 0x0080u) return 1;
-      if (a & 0x1000u) return (f8 && (a & 0x1FFEu) == 0x1FF8u) ? 0 : 2;
+      if (a & 0x1000u) return hot(a & 0xFFFu) ? 0 : 2;
       if (!(a & 0x1080u)) return 3;
       if ((a & 0x1284u) == 0x0284u) return 4;
       return 0;
@@ -115,7 +118,7 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, bool f8, const ui
     if (!(a & 0x1000u)) return 0;
     const uint32_t lo = a & 0xFFFu;
     if (lo + 255u > 0xFFFu) return 0;
-    if (f8 && lo + 255u >= 0xFF8u) return 0;
+    if (nbanks > 1u && lo + 255u >= hs) return 0;
     return 2;
   };
   // the fall-through PC must stay inside the window (its low 12 bits are stored)
@@ -196,10 +199,10 @@ inline void predecode_roms(const uint8_t* img, const uint32_t* rom_off, const ui
   uint64_t stab[256];
   build_scalar_table(stab);
   for (int r = 0; r < n_roms; ++r) {
-    const bool f8 = rom_len[r] == 8192u;
-    for (uint32_t b = 0; b < rom_len[r] / 4096u; ++b) {
+    const uint32_t nb = rom_len[r] / 4096u;
+    for (uint32_t b = 0; b < nb; ++b) {
       const uint8_t* bank = img + rom_off[r] + 4096u * b;
-      for (uint32_t o = 0; o < 4096u; ++o) rec[rom_off[r] + 4096u * b + o] = predecode_one(bank, o, f8, stab);
+      for (uint32_t o = 0; o < 4096u; ++o) rec[rom_off[r] + 4096u * b + o] = predecode_one(bank, o, nb, stab);
     }
   }
 }

@@ -162,7 +162,7 @@ def test_static_frames_raw(case):
     run_parity(gpu, ref, 6)
 
 
-def _random_states(n, n_roms, rng):
+def _random_states(n, n_roms, rng, banks=None):
     """Valid random snapshots (canonical field ranges) for single-instruction
     cross-checks."""
     s = np.zeros((n, 256), np.uint8)
@@ -170,7 +170,10 @@ def _random_states(n, n_roms, rng):
     s[:, 4] = (rng.integers(0, 256, n) & ~0x10) | 0x20
     rom_id = rng.integers(0, n_roms, n)
     s[:, 61] = rom_id
-    s[:, 5] = np.where(rom_id >= 2, rng.integers(0, 2, n), 0)         # ROMs 2,3 are F8
+    if banks is None:
+        s[:, 5] = np.where(rom_id >= 2, rng.integers(0, 2, n), 0)     # ROMs 2,3 are F8
+    else:                                                             # banks of each ROM
+        s[:, 5] = (rng.integers(0, 8, n) % np.asarray(banks)[rom_id]).astype(np.uint8)
     pcs = np.where(rng.random(n) < 0.9, rng.integers(0xF000, 0x10000, n),
                    rng.integers(0x80, 0x100, n))
     pcs = np.where(rng.random(n) < 0.02, rng.integers(0, 0x10000, n), pcs)
@@ -243,6 +246,56 @@ def test_random_instructions(n_instr, engine):
         raise AssertionError(f"{len(bad)}+ mismatches; env {i} op {op} pc {H.pc(st[i]):04x} status "
                              f"gpu {status[i]} oracle {r}; bytes {cols.tolist()[:12]} gpu "
                              f"{got[i][cols].tolist()[:12]} oracle {s[cols].tolist()[:12]}")
+
+
+@pytest.mark.parametrize("n_instr", [1, 40])
+def test_mapper_random_instructions(n_instr, engine):
+    """NEXT-4 mappers: random instructions on random 2K / F6 / F4 cartridges (hotspots at
+    $1FF6-$1FF9 and $1FF4-$1FFB, the 2K mirror) through the debug entry, against the oracle.
+    The scalar engine takes 2K + F6 (its records must fit in shared memory); F4 runs on the
+    batched engine."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    rng = np.random.default_rng(500 + n_instr)
+    sizes = [2048, 16384] if engine == "scalar" else [2048, 16384, 32768]
+    roms = [rng.integers(0, 256, n, dtype=np.uint8).tobytes() for n in sizes]
+    banks = [max(1, n // 4096) for n in sizes]
+    n = 60_000 if n_instr == 1 else 12_000
+    gpu = Env(roms, n, 1, obs_mode="raw", reset_cache_size=1, startup_frames=0, max_random_frames=0)
+    check_engine(gpu)
+    st = _random_states(n, len(roms), rng, banks)
+    gpu.set_state(st)
+    status = gpu.debug_exec(n_instr).cpu().numpy()
+    got = gpu.get_state()
+    bad = []
+    for i in range(n):
+        s = st[i].copy()
+        r, _ = oracle.exec_instr(roms[st[i, 61]], s, n_instr)
+        if r != status[i] or not (s == got[i]).all():
+            bad.append(i)
+            if len(bad) > 5:
+                break
+    assert not bad, f"{len(bad)}+ mismatches, first env {bad[0]} rom {st[bad[0], 61]} pc {H.pc(st[bad[0]]):04x}"
+
+
+@pytest.mark.parametrize("nbanks", [4, 8])
+def test_m22_bank_programs(nbanks, engine):
+    """The F6 / F4 micro-programs (oracle pins in test_oracle_riot_cart.py) give the same state
+    on the GPU after every step of 37 instructions."""
+    import oracle
+    from paper_1907_08467_b200 import Env
+    if engine == "scalar" and nbanks == 8:
+        pytest.skip("F4 records do not fit the scalar engine's shared memory (batched engine runs it)")
+    rom = micro.build(micro.m22_banks(nbanks), 4096 * nbanks)
+    gpu = Env([rom], 3, 1, obs_mode="raw", reset_cache_size=1, startup_frames=0, max_random_frames=0)
+    check_engine(gpu)
+    s0 = np.stack([oracle.power_on(rom)] * 3)
+    gpu.set_state(s0)
+    for _ in range(10):
+        gpu.debug_exec(37)
+        for i in range(3):
+            oracle.exec_instr(rom, s0[i], 37)
+        assert_same_state(gpu.get_state(), s0, "m22")
 
 
 def test_set_state_windowed_parity():

@@ -23,11 +23,11 @@ CSRC = os.path.join(ROOT, "paper_1907_08467_b200", "csrc")
 
 SHIM = r"""
 #include "scalar_predecode.h"
-extern "C" unsigned long long pd_one(const unsigned char* bank, unsigned o, int f8) {
+extern "C" unsigned long long pd_one(const unsigned char* bank, unsigned o, int nbanks) {
   static uint64_t stab[256];
   static bool init = false;
   if (!init) { cule::build_scalar_table(stab); init = true; }
-  return cule::predecode_one(bank, o, f8 != 0, stab);
+  return cule::predecode_one(bank, o, (uint32_t)nbanks, stab);
 }
 extern "C" int pd_class(const char* name) {
   // the class numbering, by name, so the test does not hard-code the enum
@@ -64,10 +64,10 @@ def pd():
                "ROR INR ASLA LSRA ROLA RORA NOP BR JMP".split()}
 
         @staticmethod
-        def rec(code, o=0x100, f8=False, size=4096):
+        def rec(code, o=0x100, f8=False, size=4096, nbanks=None):
             bank = bytearray(size)
             bank[o:o + len(code)] = bytes(code)
-            v = L.pd_one(bytes(bank), o, 1 if f8 else 0)
+            v = L.pd_one(bytes(bank), o, nbanks if nbanks is not None else (2 if f8 else 1))
             lo, hi = v & 0xFFFFFFFF, v >> 32
             return dict(cls=lo & 31, aux=(lo >> 5) & 7, cyc=(lo >> 8) & 15, nxt=lo >> 20, hi=hi)
     assert all(v >= 0 for v in P.cls.values())
@@ -158,3 +158,15 @@ def test_window_rules(pd):
     assert pd.rec([0xAD, 0xF8, 0xFF], f8=True)["cls"] == c["GEN"]           # LDA $FFF8 switches banks
     assert pd.rec([0xAD, 0xF8, 0xFF], f8=False)["cls"] == c["LD"]
     assert pd.rec([0xB9, 0x00, 0xFF], f8=True)["cls"] == c["GEN"]           # abs,Y can reach $FFF8
+    # F6 ($FF6-$FF9) and F4 ($FF4-$FFB) hotspot windows
+    assert pd.rec([0xEA], o=0xFF6, nbanks=4)["cls"] == c["GEN"]
+    assert pd.rec([0xEA], o=0xFF6, nbanks=2)["cls"] == c["NOP"]
+    assert pd.rec([0xEA], o=0xFF4, nbanks=8)["cls"] == c["GEN"]
+    assert pd.rec([0xEA], o=0xFFB, nbanks=8)["cls"] == c["GEN"]
+    assert pd.rec([0xEA], o=0xFFA, nbanks=4)["cls"] == c["NOP"]
+    assert pd.rec([0xAD, 0xF6, 0xFF], nbanks=4)["cls"] == c["GEN"]        # LDA $FFF6 switches (F6)
+    assert pd.rec([0xAD, 0xF5, 0xFF], nbanks=4)["cls"] == c["LD"]
+    assert pd.rec([0xAD, 0xFB, 0xFF], nbanks=8)["cls"] == c["GEN"]        # LDA $FFFB switches (F4)
+    assert pd.rec([0xB9, 0x00, 0xFF], nbanks=8)["cls"] == c["GEN"]        # abs,Y can reach $FFF4
+    assert pd.rec([0xB9, 0x00, 0xFF], nbanks=1)["cls"] == c["LD"]
+    assert pd.rec([0xB9, 0xF0, 0xFE], nbanks=8)["cls"] == c["LD"]         # ends at $FFEF: clear
