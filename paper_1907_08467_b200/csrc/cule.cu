@@ -199,8 +199,9 @@ static uint32_t choose_block(uint32_t warps) {
     int b = atoi(v);
     if (b == 32 || b == 64 || b == 128) return (uint32_t)b;
   }
+  // measured at 32768 envs (epw 32): 128 threads 2.90M FPS, 64 2.86M, 32 2.02M
   uint32_t b = 128;
-  while (b > 32 && (warps * 32u + b - 1) / b < 2u * (uint32_t)sm_count()) b /= 2;
+  while (b > 32 && (warps * 32u + b - 1) / b < (uint32_t)sm_count()) b /= 2;
   return b;
 }
 
