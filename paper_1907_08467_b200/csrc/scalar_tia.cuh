@@ -243,7 +243,7 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
 }
 
 // shaded colour cache: 4 words (COLUP0, COLUP1, COLUPF, COLUBK) right after the warp's ring;
-// every lane writes the same word, so each lane's later reads see it without a barrier
+// every lane writes the same word, followed by a warp barrier before the next reads
 constexpr uint32_t kShadeOff = 480;
 __device__ __forceinline__ void shade_store(uint32_t a, uint32_t colu, const uint8_t* gray) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(Tia::shade(colu, gray)) : "memory");
@@ -428,7 +428,10 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
     catch_up_coop(t, T, rb, lane, ystart, gray, w, dirty);
     __syncwarp();  // reconverge: the register update is warp-uniform work, issued once
     t.apply(r, e & 0xFFu, T);
-    if (r - 6u < 4u) shade_store(rb.ring_s + kShadeOff + 4u * (r - 6u), e & 0xFFu, gray);  // COLUxx
+    if (r - 6u < 4u) {  // COLUxx: refresh the shaded colour, ordered before any lane's next read
+      shade_store(rb.ring_s + kShadeOff + 4u * (r - 6u), e & 0xFFu, gray);
+      __syncwarp();
+    }
     dirty |= kDirtyTable.v[r];
   }
   if (fin) catch_up_coop(t, t_final, rb, lane, ystart, gray, w, dirty);
