@@ -617,9 +617,11 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             const int32_t et = (int32_t)now - tW;
             const uint32_t tV = tVS & 0xFFu, tS = (tVS >> 8) & 0xFFu, tm = tVS >> 16;  // tm = 2^tS - 1
             const int32_t VI = (int32_t)(tV << tS);
-            if (hi & 1u) v = et > VI ? 0x80u : 0u;  // TIMINT
-            else if (et <= VI) v = (tV - (uint32_t)((et + (int32_t)tm) >> tS)) & 0xFFu;
-            else v = (uint32_t)(0xFF - (et - VI - 1)) & 0xFFu;
+            // branch-free: INTIM while counting / after expiry (0xFF - (e - VI - 1) = VI - e mod 256), TIMINT
+            const bool expired = et > VI;
+            const uint32_t counting = (tV - (uint32_t)((et + (int32_t)tm) >> tS)) & 0xFFu;
+            const uint32_t intim = expired ? ((uint32_t)(VI - et) & 0xFFu) : counting;
+            v = (hi & 1u) ? (expired ? 0x80u : 0u) : intim;
             if (kSkip) {  // cycles over which the value read stays the same
               uint32_t ff = 0u;
               if (hi & 1u) ff = et > VI ? 0x7FFFFFFFu : (uint32_t)(VI - et);
