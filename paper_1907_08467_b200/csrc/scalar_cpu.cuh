@@ -635,8 +635,9 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
             nz = (A & v) | ((v & 0x80u) << 8);  // C_TBIT
             V = (v >> 6) & 1u;
           } break;
-          case C_STTIA: {
-            const uint32_t wv = aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X)));
+          case C_LDA: if (!rd_operand()) CULE_FALLBACK(); A = v; setnz(v); break;
+          case C_STATIA: case C_STTIA: {
+            const uint32_t wv = cls == C_STATIA ? A : (aux == 0u ? A : (aux == 1u ? X : (aux == 2u ? Y : (A & X))));
             st_log(lg0 + 4u * log_len, ((3u * now) << 14) | hi | wv);
             ++log_len;
             if (log_len > log_lim) {
@@ -678,7 +679,6 @@ __device__ __forceinline__ uint32_t run_cpu(SMach* M, uint32_t rom_all0, uint32_
           case C_EOR: if (!rd_operand()) CULE_FALLBACK(); A ^= v; setnz(A); break;
           case C_ADC: if (!rd_operand()) CULE_FALLBACK(); adc(v); break;
           case C_BIT: if (!rd_operand()) CULE_FALLBACK(); nz = (A & v) | ((v & 0x80u) << 8); V = (v >> 6) & 1u; break;
-          case C_NOPR: if (!rd_operand()) CULE_FALLBACK(); break;
           case C_STRAM: {
             const uint32_t t = ea_t();
             if (!(t & 0x80u)) CULE_FALLBACK();

@@ -50,8 +50,10 @@ enum PClass : uint32_t {
   // offset of the operand byte); AUX = register (C_CMP: 0 A 1 X 2 Y, C_LD: bit mask 1 A 2 X 4 Y)
   // -- the classes most frequent after C_BR come first (1..C_HOT_LAST): the kernel dispatches
   //    them through a separate, smaller switch
+  C_LDA,    // LDA (C_LD with AUX = 1): A only
+  C_STATIA, // STA to a TIA effect register (C_STTIA with AUX = 0)
   C_LD, C_STTIA, C_TLD, C_TBIT, C_TR, C_CMP, C_FLAG, C_SBC, C_WSYNC,
-  C_ORA, C_AND, C_EOR, C_ADC, C_BIT, C_NOPR,
+  C_ORA, C_AND, C_EOR, C_ADC, C_BIT,
   C_STRAM,  // store to RAM (zero page, zp indexed, or absolute RAM); AUX 0 A 1 X 2 Y 3 A&X
   C_INC, C_DEC, C_ASL, C_LSR, C_ROL, C_ROR,  // read-modify-write of RAM
   C_INR,    // INX/INY/DEX/DEY, AUX as K_INR
@@ -135,7 +137,8 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, uint32_t nbanks, 
         if (kind == K_NOP && len == 1) { cls = C_NOP; break; }
         const uint32_t rcls = kind == K_ORA ? C_ORA : kind == K_AND ? C_AND : kind == K_EOR ? C_EOR :
                               kind == K_ADC ? C_ADC : kind == K_SBC ? C_SBC : kind == K_CMP ? C_CMP :
-                              kind == K_BIT ? C_BIT : kind == K_LD ? C_LD : C_NOPR;
+                              kind == K_BIT ? C_BIT : kind == K_LD ? ((aux & 7u) == 1u ? C_LDA : C_LD) : C_GEN;
+        if (rcls == C_GEN) break;  // NOP reads: general path (rare)
         raux = aux & 7u;
         if (imm) { mem(rcls, o + 1, false); break; }
         const int w = where();
@@ -153,7 +156,7 @@ inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, uint32_t nbanks, 
           const uint32_t r = (zp ? b1 : base) & 0x3Fu;
           // TIA writes with a picture effect: 0x01, 0x04-0x14, 0x1B-0x2C (scalar_cpu.cuh kTiaEffect)
           const bool eff = r == 0x01u || (r >= 0x04u && r <= 0x14u) || (r >= 0x1Bu && r <= 0x2Cu);
-          if (eff) { cls = C_STTIA; hi = r << 8; }
+          if (eff) { cls = raux == 0u ? C_STATIA : C_STTIA; hi = r << 8; }
           else if (r == 0x02u) cls = C_WSYNC;
         }
         break;

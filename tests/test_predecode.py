@@ -35,7 +35,8 @@ extern "C" int pd_class(const char* name) {
     {"GEN", cule::C_GEN}, {"LD", cule::C_LD}, {"STTIA", cule::C_STTIA}, {"TLD", cule::C_TLD},
     {"TBIT", cule::C_TBIT}, {"TR", cule::C_TR}, {"CMP", cule::C_CMP}, {"FLAG", cule::C_FLAG},
     {"SBC", cule::C_SBC}, {"WSYNC", cule::C_WSYNC}, {"ORA", cule::C_ORA}, {"AND", cule::C_AND},
-    {"EOR", cule::C_EOR}, {"ADC", cule::C_ADC}, {"BIT", cule::C_BIT}, {"NOPR", cule::C_NOPR},
+    {"EOR", cule::C_EOR}, {"ADC", cule::C_ADC}, {"BIT", cule::C_BIT}, {"LDA", cule::C_LDA},
+    {"STATIA", cule::C_STATIA},
     {"STRAM", cule::C_STRAM}, {"INC", cule::C_INC}, {"DEC", cule::C_DEC}, {"ASL", cule::C_ASL},
     {"LSR", cule::C_LSR}, {"ROL", cule::C_ROL}, {"ROR", cule::C_ROR}, {"INR", cule::C_INR},
     {"ASLA", cule::C_ASLA}, {"LSRA", cule::C_LSRA}, {"ROLA", cule::C_ROLA}, {"RORA", cule::C_RORA},
@@ -60,7 +61,7 @@ def pd():
 
     class P:
         cls = {n: L.pd_class(n.encode()) for n in
-               "GEN LD STTIA TLD TBIT TR CMP FLAG SBC WSYNC ORA AND EOR ADC BIT NOPR STRAM INC DEC ASL LSR ROL "
+               "GEN LDA STATIA LD STTIA TLD TBIT TR CMP FLAG SBC WSYNC ORA AND EOR ADC BIT STRAM INC DEC ASL LSR ROL "
                "ROR INR ASLA LSRA ROLA RORA NOP BR JMP".split()}
 
         @staticmethod
@@ -102,7 +103,8 @@ def test_lengths_cycles_and_page_cross_match_the_opcode_matrix(pd):
             assert r["hi"] & 0xFFF == 0x102 + 0x10
         else:
             assert r["cyc"] == e["base"], (hex(op), r["cyc"], e["base"])
-        if r["cls"] not in (pd.cls["BR"], pd.cls["STTIA"], pd.cls["TLD"], pd.cls["TBIT"], pd.cls["TR"], pd.cls["JMP"]):
+        if r["cls"] not in (pd.cls["BR"], pd.cls["STTIA"], pd.cls["STATIA"], pd.cls["TLD"], pd.cls["TBIT"], pd.cls["TR"],
+                            pd.cls["JMP"]):
             pen = bool(r["hi"] & 0x100)
             assert pen == (e["plus"] and e["mode"] in ("ax", "ay")), hex(op)  # (zp),Y is general path
     assert fast >= 120
@@ -110,14 +112,17 @@ def test_lengths_cycles_and_page_cross_match_the_opcode_matrix(pd):
 
 def test_classes_of_common_instructions(pd):
     c = pd.cls
-    assert pd.rec([0xA9, 0x12])["cls"] == c["LD"]                          # LDA #
-    assert pd.rec([0xA5, 0x85])["cls"] == c["LD"]                          # LDA zp (RAM)
+    assert pd.rec([0xA9, 0x12])["cls"] == c["LDA"]                         # LDA #
+    assert pd.rec([0xA5, 0x85])["cls"] == c["LDA"]                         # LDA zp (RAM)
+    assert pd.rec([0xA2, 0x12])["cls"] == c["LD"]                          # LDX #
+    assert pd.rec([0x04, 0x85])["cls"] == c["GEN"]                         # NOP zp (read): general path
     assert pd.rec([0xA5, 0x05])["cls"] == c["GEN"]                         # LDA zp (TIA read)
     assert pd.rec([0xAD, 0x84, 0x02])["cls"] == c["TLD"]                   # LDA INTIM
     assert pd.rec([0x2C, 0x85, 0x02])["cls"] == c["TBIT"]                  # BIT TIMINT
     assert pd.rec([0xAD, 0x80, 0x02])["cls"] == c["GEN"]                   # LDA SWCHA (RIOT I/O)
     r = pd.rec([0x85, 0x1B])                                               # STA GRP0
-    assert r["cls"] == c["STTIA"] and r["hi"] == 0x1B << 8
+    assert r["cls"] == c["STATIA"] and r["hi"] == 0x1B << 8
+    assert pd.rec([0x86, 0x1B])["cls"] == c["STTIA"]                       # STX GRP0
     assert pd.rec([0x85, 0x02])["cls"] == c["WSYNC"]                       # STA WSYNC
     assert pd.rec([0x8D, 0x02, 0x01])["cls"] == c["WSYNC"]                 # STA $0102 (mirror)
     assert pd.rec([0x85, 0x00])["cls"] == c["GEN"]                         # STA VSYNC
@@ -125,9 +130,9 @@ def test_classes_of_common_instructions(pd):
     r = pd.rec([0x85, 0x85])                                               # STA zp RAM
     assert r["cls"] == c["STRAM"] and r["hi"] >> 31 == 1
     r = pd.rec([0xB9, 0xF0, 0x00])                                         # LDA $00F0,Y: RAM-based abs,Y
-    assert r["cls"] == c["LD"] and r["hi"] >> 31 == 1 and (r["hi"] >> 16) & 0xFFF == 0xF0
+    assert r["cls"] == c["LDA"] and r["hi"] >> 31 == 1 and (r["hi"] >> 16) & 0xFFF == 0xF0
     r = pd.rec([0xB9, 0x00, 0xF3])                                         # LDA $F300,Y: cartridge table
-    assert r["cls"] == c["LD"] and r["hi"] >> 31 == 0 and (r["hi"] >> 16) & 0xFFF == 0x300
+    assert r["cls"] == c["LDA"] and r["hi"] >> 31 == 0 and (r["hi"] >> 16) & 0xFFF == 0x300
     assert pd.rec([0xB9, 0x80, 0xFF])["cls"] == c["GEN"]                   # abs,Y past the window end
     assert pd.rec([0x4C, 0x00, 0xF0])["cls"] == c["JMP"]                   # JMP $F000
     assert pd.rec([0x4C, 0x80, 0x00])["cls"] == c["GEN"]                   # JMP into RAM
@@ -156,7 +161,7 @@ def test_window_rules(pd):
     assert pd.rec([0xAD, 0x84, 0x02], o=0xFF6, f8=True)["cls"] == c["GEN"]
     assert pd.rec([0xAD, 0x84, 0x02], o=0xFF6, f8=False)["cls"] == c["TLD"]
     assert pd.rec([0xAD, 0xF8, 0xFF], f8=True)["cls"] == c["GEN"]           # LDA $FFF8 switches banks
-    assert pd.rec([0xAD, 0xF8, 0xFF], f8=False)["cls"] == c["LD"]
+    assert pd.rec([0xAD, 0xF8, 0xFF], f8=False)["cls"] == c["LDA"]
     assert pd.rec([0xB9, 0x00, 0xFF], f8=True)["cls"] == c["GEN"]           # abs,Y can reach $FFF8
     # F6 ($FF6-$FF9) and F4 ($FF4-$FFB) hotspot windows
     assert pd.rec([0xEA], o=0xFF6, nbanks=4)["cls"] == c["GEN"]
@@ -165,8 +170,8 @@ def test_window_rules(pd):
     assert pd.rec([0xEA], o=0xFFB, nbanks=8)["cls"] == c["GEN"]
     assert pd.rec([0xEA], o=0xFFA, nbanks=4)["cls"] == c["NOP"]
     assert pd.rec([0xAD, 0xF6, 0xFF], nbanks=4)["cls"] == c["GEN"]        # LDA $FFF6 switches (F6)
-    assert pd.rec([0xAD, 0xF5, 0xFF], nbanks=4)["cls"] == c["LD"]
+    assert pd.rec([0xAD, 0xF5, 0xFF], nbanks=4)["cls"] == c["LDA"]
     assert pd.rec([0xAD, 0xFB, 0xFF], nbanks=8)["cls"] == c["GEN"]        # LDA $FFFB switches (F4)
     assert pd.rec([0xB9, 0x00, 0xFF], nbanks=8)["cls"] == c["GEN"]        # abs,Y can reach $FFF4
-    assert pd.rec([0xB9, 0x00, 0xFF], nbanks=1)["cls"] == c["LD"]
-    assert pd.rec([0xB9, 0xF0, 0xFE], nbanks=8)["cls"] == c["LD"]         # ends at $FFEF: clear
+    assert pd.rec([0xB9, 0x00, 0xFF], nbanks=1)["cls"] == c["LDA"]
+    assert pd.rec([0xB9, 0xF0, 0xFE], nbanks=8)["cls"] == c["LDA"]        # ends at $FFEF: clear
