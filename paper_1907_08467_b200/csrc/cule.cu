@@ -173,8 +173,8 @@ static int choose_engine(int N) {
     if (!strcmp(v, "simt")) return 0;
     if (!strcmp(v, "scalar")) return 1;
   }
-  // measured (profiles/r01_v6_engine_sweep.txt): 4096 envs scalar 2.70M vs SIMT 0.73M FPS;
-  // 16384 (F8) 2.65M vs 2.27M; 32768 (4 ROMs) 2.06M vs 2.77M
+  // measured (profiles/r01_v6_engine_sweep.txt): 4096 envs scalar 2.81M vs SIMT 0.74M FPS;
+  // 16384 (F8) 2.72M vs 2.30M; 32768 (4 ROMs) 2.09M vs 2.87M
   return N <= 16384 ? 1 : 0;
 }
 
