@@ -75,3 +75,26 @@ def test_vtrace_rejects_bad_arguments():
         vtrace(**dev, gamma=1.5)
     with pytest.raises(ValueError):
         vtrace(**{**dev, "dones": dev["dones"].float()}, gamma=0.9)
+
+
+def test_vtrace_sampled_at_bench_size():
+    """The bench's HBM-roofline shape (T=20, B=2^20, 64-thread blocks across every SM): 200
+    sampled trajectories against the oracle."""
+    from oracle import vtrace as VT
+    from paper_1907_08467_b200.vtrace import vtrace
+    T, B = 20, 1 << 20
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    tr = dict(rewards=torch.randn(T, B, device="cuda", generator=g), values=torch.randn(T, B, device="cuda", generator=g),
+              bootstrap=torch.randn(B, device="cuda", generator=g),
+              log_mu=torch.randn(T, B, device="cuda", generator=g) * 0.5,
+              log_pi=torch.randn(T, B, device="cuda", generator=g) * 0.5,
+              dones=(torch.rand(T, B, device="cuda", generator=g) < 0.05).to(torch.uint8))
+    vs, rho, adv = vtrace(**tr, gamma=0.99)
+    cols = np.random.default_rng(0).choice(B, 200, replace=False)
+    sub = {k: (v[..., cols] if v.dim() == 2 else v[cols]).cpu().numpy() for k, v in tr.items()}
+    ref = VT.vtrace_recursive(**{k: v.astype(np.float64) if v.dtype != np.uint8 else v for k, v in sub.items()},
+                              gamma=np.float32(0.99).item(), rho_bar=1.0, c_bar=1.0)
+    M = max(np.abs(sub["rewards"]).max(), np.abs(sub["values"]).max(), np.abs(ref[0]).max())
+    for got, want in zip((vs, rho, adv), ref):
+        assert np.abs(got[:, cols].cpu().numpy().astype(np.float64) - want).max() <= 2e-6 * T * (1 + M)
