@@ -23,6 +23,11 @@
  *     memory;
  *   - calls taking `cuda_stream` (a cudaStream_t, NULL = legacy default stream) are asynchronous
  *     on that stream unless stated; a sticky CUDA error surfaces as CULE_E_CUDA on a later call;
+ *   - every call on a handle runs on the device that was current at cule_create (the library
+ *     switches to it and restores the caller's device on return); `cuda_stream` must belong to
+ *     that device;
+ *   - one handle is used from one stream at a time: calls on the same handle must not be in
+ *     flight on two streams at once (they share the workspace: state, staging, work tickets);
  *   - per-environment runtime faults (JAM / unstable opcode, runaway frame) are data, not call
  *     errors: the env reports done = 1 with reward 0 and an all-zero observation, is reset from
  *     the cache, and the `faults` counter is incremented.
@@ -137,7 +142,10 @@ int cule_step_host(cule_env* env, const uint8_t* h_actions, void* h_obs, int32_t
                    uint8_t* h_dones, void* cuda_stream);
 
 /* Copy the packed snapshots u8[N][256] to / from HOST memory.  Synchronous
- * with respect to cuda_stream. */
+ * with respect to cuda_stream.  cule_set_state validates every snapshot on the host before
+ * anything is uploaded and returns CULE_E_INVAL (state unchanged) if any has rom_id >= n_roms,
+ * a bank outside its ROM, a timer shift not in {0,3,6,10}, an object position >= 160, fc at or
+ * beyond the line cap (76 * line_cap cycles) or a fault code > 2. */
 int cule_get_state(cule_env* env, uint8_t* h_states, void* cuda_stream);
 int cule_set_state(cule_env* env, const uint8_t* h_states, void* cuda_stream);
 

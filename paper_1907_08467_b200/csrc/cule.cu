@@ -146,8 +146,23 @@ static bool live(const cule_env* e) {
   return e && g_live.count(e);
 }
 
+// Every handle call runs on the handle's device (its workspace lives there), whatever device
+// the calling thread has current; the previous device is restored on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 #define CHECK_LIVE(e) \
-  do { if (!live(e)) return fail(CULE_E_CLOSED, "invalid or destroyed cule_env handle"); } while (0)
+  do { if (!live(e)) return fail(CULE_E_CLOSED, "invalid or destroyed cule_env handle"); } while (0); \
+  DeviceGuard device_guard_((e)->device)
 
 static int cuda_check(const char* what) {
   cudaError_t err = cudaGetLastError();
@@ -435,6 +450,9 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
   p.dones = d_dones;
   if (e->engine == 1) {
     const uint32_t sg = e->sgrid;
+    // the persistent kernel's work tickets start from zero on the launch stream (the kernel also
+    // re-zeroes them when it finishes; this covers an aborted launch)
+    cudaMemsetAsync(e->ws + e->L.tickets, 0, 16, s);
     if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::scalar_kernel<true, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
     else cule::scalar_kernel<false, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
   } else if (e->cfg.obs_mode == CULE_OBS_GRAY84) {
@@ -492,11 +510,34 @@ int cule_get_state(cule_env* e, uint8_t* h_states, void* stream) {
   return cuda_check("cule_get_state");
 }
 
+// A snapshot indexes shared-memory ROM/record images (rom_id, bank) and the reset cache
+// (rom_id), and the renderer assumes positions in [0, 160): reject anything outside the model
+// before it reaches the device.
+static int validate_snapshot(const cule_env* e, const uint8_t* s, size_t i) {
+  // rom_id must name one of this handle's ROMs (a get_state snapshot carries rom (env_index_base+i)
+  // % n_roms; the single-instruction tests load other valid ids on purpose)
+  const uint32_t rom = s[61];
+  const std::string at = "snapshot of env " + std::to_string(i) + ": ";
+  if (rom >= (uint32_t)e->n_roms) return fail(CULE_E_INVAL, at + "rom_id " + std::to_string(rom) + " >= n_roms");
+  if (s[5] >= cule::banks_of(e->rom_banks, rom)) return fail(CULE_E_INVAL, at + "bank out of range for its ROM");
+  if (s[17] != 0 && s[17] != 3 && s[17] != 6 && s[17] != 10) return fail(CULE_E_INVAL, at + "timer shift not in {0,3,6,10}");
+  for (int k = 56; k <= 60; ++k)
+    if (s[k] >= 160) return fail(CULE_E_INVAL, at + "object position >= 160");
+  const uint32_t fc = (uint32_t)s[8] | ((uint32_t)s[9] << 8) | ((uint32_t)s[10] << 16) | ((uint32_t)s[11] << 24);
+  if (fc >= 76u * (uint32_t)e->cfg.line_cap) return fail(CULE_E_INVAL, at + "fc beyond the line cap");
+  if (s[62] > 2) return fail(CULE_E_INVAL, at + "fault code not in {0,1,2}");
+  return CULE_OK;
+}
+
 int cule_set_state(cule_env* e, const uint8_t* h_states, void* stream) {
   CHECK_LIVE(e);
   if (!h_states) return fail(CULE_E_INVAL, "null buffer");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t n = (size_t)e->N;
+  for (size_t i = 0; i < n; ++i) {
+    const int rc = validate_snapshot(e, h_states + 256 * i, i);
+    if (rc) return rc;
+  }
   cudaMemcpyAsync(e->ws + e->L.pack, h_states, 256 * n, cudaMemcpyHostToDevice, s);
   cule::unpack_kernel<<<(unsigned)((n * 16 + 255) / 256), 256, 0, s>>>(e->ws + e->L.state, e->ws + e->L.pack, (uint32_t)n);
   cudaStreamSynchronize(s);
@@ -519,6 +560,7 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
   p.debug_status = d_status;
   if (e->engine == 1) {
     const uint32_t sg = e->sgrid;
+    cudaMemsetAsync(e->ws + e->L.tickets, 0, 16, static_cast<cudaStream_t>(stream));
     cule::scalar_kernel<false, true><<<sg, 32 * cule::kSWarps, e->ssmem, static_cast<cudaStream_t>(stream)>>>(p);
   } else {
     cule::debug_kernel<<<e->grid, e->block, e->smem, static_cast<cudaStream_t>(stream)>>>(p);

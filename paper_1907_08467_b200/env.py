@@ -15,8 +15,8 @@ from . import _lib
 from .inputs import palette as _palette
 
 
-def _stream_ptr(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_ptr(stream=None, device=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
 
 
@@ -36,11 +36,16 @@ class Env:
         roms = [bytes(r) for r in roms]
         self.num_envs = int(num_envs)
         self.frameskip = int(frameskip)
+        if obs_mode not in ("gray84", "raw"):
+            raise ValueError(f"obs_mode must be 'gray84' or 'raw', got {obs_mode!r}")
         c = _lib.default_config()
         c.obs_mode = _lib.CULE_OBS_GRAY84 if obs_mode == "gray84" else _lib.CULE_OBS_RAW
         c.seed = seed
         c.env_index_base = env_index_base
+        fields = {f for f, _ in _lib.CuleConfig._fields_} - {"obs_mode", "palette_rgb"}
         for k, v in cfg.items():
+            if k not in fields:
+                raise ValueError(f"unknown config key {k!r}; valid keys: {sorted(fields)}")
             setattr(c, k, v)
         self._pal = np.frombuffer(_palette.load_palette(), np.uint8).copy()
         c.palette_rgb = self._pal.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
@@ -71,10 +76,17 @@ class Env:
         self.obs_bytes = int(np.prod(shape))
         self.engine = "scalar" if _lib.check(L.cule_engine(self._h)) == 1 else "simt"
 
+    def _sp(self, stream) -> int:
+        """The caller's stream, else the current stream of the env's device (not of whatever
+        device happens to be current); the library switches to the env's device itself."""
+        if stream is not None and stream.device != self.device:
+            raise ValueError("stream must belong to the env's device")
+        return _stream_ptr(stream, self.device)
+
     # -- core calls ----------------------------------------------------------------------------
     def reset(self, seed: int = 0, stream=None) -> torch.Tensor:
         _lib.check(_lib.load().cule_reset(self._h, seed, ctypes.c_void_p(self.obs.data_ptr()),
-                                          ctypes.c_void_p(_stream_ptr(stream))))
+                                          ctypes.c_void_p(self._sp(stream))))
         return self.obs
 
     def step(self, actions: torch.Tensor, stream=None):
@@ -85,7 +97,7 @@ class Env:
                                          ctypes.c_void_p(self.obs.data_ptr()),
                                          ctypes.c_void_p(self.rewards.data_ptr()),
                                          ctypes.c_void_p(self.dones.data_ptr()),
-                                         ctypes.c_void_p(_stream_ptr(stream))))
+                                         ctypes.c_void_p(self._sp(stream))))
         return self.obs, self.rewards, self.dones
 
     # -- inference path: frame stack (R#32) ------------------
@@ -98,7 +110,7 @@ class Env:
     def reset_stacked(self, stack: torch.Tensor, seed: int = 0, stream=None) -> torch.Tensor:
         self._check_stack(stack)
         _lib.check(_lib.load().cule_reset_stacked(self._h, seed, ctypes.c_void_p(stack.data_ptr()),
-                                                  ctypes.c_void_p(_stream_ptr(stream))))
+                                                  ctypes.c_void_p(self._sp(stream))))
         return stack
 
     def step_stacked(self, actions: torch.Tensor, stack: torch.Tensor, slot: int, stream=None):
@@ -112,7 +124,7 @@ class Env:
                                                  ctypes.c_void_p(stack.data_ptr()), int(slot),
                                                  ctypes.c_void_p(self.rewards.data_ptr()),
                                                  ctypes.c_void_p(self.dones.data_ptr()),
-                                                 ctypes.c_void_p(_stream_ptr(stream))))
+                                                 ctypes.c_void_p(self._sp(stream))))
         return self.rewards, self.dones
 
     def _check_stack(self, stack: torch.Tensor) -> None:
@@ -122,17 +134,28 @@ class Env:
 
     def step_host(self, h_actions: torch.Tensor, h_obs, h_rewards: torch.Tensor,
                   h_dones: torch.Tensor, stream=None):
-        """Host-buffer step (pinned CPU tensors): copies in, steps, copies out, synchronises."""
+        """Host-buffer step (pinned CPU tensors): copies in, steps, copies out, synchronises.
+        h_actions u8[N], h_obs u8[N, *obs_shape] or None, h_rewards i32[N], h_dones u8[N]: all
+        contiguous CPU tensors (pinned recommended); the library writes exactly these sizes."""
+        n = self.num_envs
+        for name, t, dt, numel in (("h_actions", h_actions, torch.uint8, n),
+                                   ("h_obs", h_obs, torch.uint8, n * self.obs_bytes),
+                                   ("h_rewards", h_rewards, torch.int32, n), ("h_dones", h_dones, torch.uint8, n)):
+            if t is None and name == "h_obs":
+                continue
+            if (not isinstance(t, torch.Tensor) or t.device.type != "cpu" or t.dtype != dt
+                    or not t.is_contiguous() or t.numel() != numel):
+                raise ValueError(f"{name} must be a contiguous CPU {dt} tensor of {numel} elements")
         _lib.check(_lib.load().cule_step_host(
             self._h, ctypes.c_void_p(h_actions.data_ptr()),
             ctypes.c_void_p(h_obs.data_ptr() if h_obs is not None else 0),
             ctypes.c_void_p(h_rewards.data_ptr()), ctypes.c_void_p(h_dones.data_ptr()),
-            ctypes.c_void_p(_stream_ptr(stream))))
+            ctypes.c_void_p(self._sp(stream))))
 
     def get_state(self, stream=None) -> np.ndarray:
         out = np.zeros((self.num_envs, _lib.STATE_BYTES), np.uint8)
         _lib.check(_lib.load().cule_get_state(self._h, ctypes.c_void_p(out.ctypes.data),
-                                              ctypes.c_void_p(_stream_ptr(stream))))
+                                              ctypes.c_void_p(self._sp(stream))))
         return out
 
     def set_state(self, states: np.ndarray, stream=None) -> None:
@@ -140,18 +163,18 @@ class Env:
         if s.shape != (self.num_envs, _lib.STATE_BYTES):
             raise ValueError("states must be u8[N, 256]")
         _lib.check(_lib.load().cule_set_state(self._h, ctypes.c_void_p(s.ctypes.data),
-                                              ctypes.c_void_p(_stream_ptr(stream))))
+                                              ctypes.c_void_p(self._sp(stream))))
 
     def counters(self, stream=None) -> torch.Tensor:
         """int64[4] on the device: frames, episodes finished, sum of episode returns, faults."""
         _lib.check(_lib.load().cule_counters(self._h, ctypes.c_void_p(self._counters.data_ptr()),
-                                             ctypes.c_void_p(_stream_ptr(stream))))
+                                             ctypes.c_void_p(self._sp(stream))))
         return self._counters
 
     def debug_exec(self, n_instr: int, stream=None) -> torch.Tensor:
         status = torch.zeros(self.num_envs, dtype=torch.int32, device=self.device)
         _lib.check(_lib.load().cule_debug_exec(self._h, n_instr, ctypes.c_void_p(status.data_ptr()),
-                                               ctypes.c_void_p(_stream_ptr(stream))))
+                                               ctypes.c_void_p(self._sp(stream))))
         return status
 
     def close(self) -> None:

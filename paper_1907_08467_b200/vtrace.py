@@ -25,10 +25,23 @@ def vtrace(rewards: torch.Tensor, values: torch.Tensor, bootstrap: torch.Tensor,
                                ("dones", dones, torch.uint8, (T, B))):
         if x.dtype != dt or not x.is_cuda or tuple(x.shape) != shape or not x.is_contiguous():
             raise ValueError(f"{name} must be a contiguous {dt} CUDA tensor of shape {shape}")
-    vs, rho, adv = out if out is not None else (torch.empty_like(rewards), torch.empty_like(rewards),
-                                                torch.empty_like(rewards))
+    dev = rewards.device
+    for name, x in (("values", values), ("bootstrap", bootstrap), ("log_mu", log_mu), ("log_pi", log_pi),
+                    ("dones", dones)):
+        if x.device != dev:
+            raise ValueError(f"{name} must be on {dev}")
+    if out is not None:
+        if len(out) != 3:
+            raise ValueError("out must be (vs, rho, adv)")
+        for name, x in zip(("vs", "rho", "adv"), out):
+            if x.dtype != torch.float32 or x.device != dev or tuple(x.shape) != (T, B) or not x.is_contiguous():
+                raise ValueError(f"out {name} must be a contiguous float32 tensor [T, B] on {dev}")
+        vs, rho, adv = out
+    else:
+        vs, rho, adv = torch.empty_like(rewards), torch.empty_like(rewards), torch.empty_like(rewards)
     p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-    _lib.check(_lib.load().cule_vtrace(p(rewards), p(values), p(bootstrap), p(log_mu), p(log_pi), p(dones),
-                                       T, B, gamma, rho_bar, c_bar, p(vs), p(rho), p(adv),
-                                       ctypes.c_void_p(_stream_ptr(stream))))
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().cule_vtrace(p(rewards), p(values), p(bootstrap), p(log_mu), p(log_pi), p(dones),
+                                           T, B, gamma, rho_bar, c_bar, p(vs), p(rho), p(adv),
+                                           ctypes.c_void_p(_stream_ptr(stream, dev))))
     return vs, rho, adv

@@ -53,3 +53,17 @@ def test_host_only_calls():
     rc = L.cule_create(None, None, 1, 16, 4, ctypes.byref(c), None, 0, ctypes.byref(out))
     assert rc == _lib.CULE_E_INVAL and b"null" in L.cule_last_error()
     assert L.cule_destroy(ctypes.c_void_p(12345)) == _lib.CULE_E_CLOSED
+
+
+def test_env_rejects_bad_config_before_touching_the_gpu():
+    # unknown config keys and obs modes are errors, not silently ignored
+    import pytest
+    from paper_1907_08467_b200 import Env
+    from paper_1907_08467_b200.inputs import games
+    rom = games.build_rom("R1")
+    with pytest.raises(ValueError, match="obs_mode"):
+        Env([rom], 4, 4, obs_mode="Gray84", device="cuda:0")
+    with pytest.raises(ValueError, match="unknown config key 'idle_skp'"):
+        Env([rom], 4, 4, device="cuda:0", idle_skp=1)
+    with pytest.raises(ValueError, match="CUDA device only"):
+        Env([rom], 4, 4, device="cpu")
