@@ -87,3 +87,32 @@ def test_gloo_counter_allreduce():
         assert local == [100 * (rank + 1), rank, -5 * rank, rank % 2]  # input untouched
         assert m == 1.5 + (world - 1)             # max over ranks
         assert (base, n) == (4096 * rank, 4096)
+
+
+def test_oracle_pool_reproduces_one_process(orc):
+    """tests/oracle_pool.py (the parallel oracle of the full-size GPU parity tests): chunks of
+    global ids replayed in separate processes equal one sequential N-env oracle run, and a
+    windowed replay from mid-run snapshots equals the continuation of that run."""
+    import oracle_pool as OP
+    roms = [games.build_rom("R1"), games.build_rom("R3")]
+    N, T = 12, 16
+    acts = H.random_actions(N, T, 8)
+    full = orc.OracleEnv(roms, N, 4, H.palette_rgb(), reset_cache_size=3, max_episode_frames=20)
+    full.reset(1)
+    ref, st8 = [], None
+    for t in range(T):
+        if t == 8:
+            st8 = full.get_state()
+        ref.append(full.step(acts[t]))
+    ids = np.array([0, 3, 4, 7, 11])
+    cfg = dict(reset_cache_size=3, max_episode_frames=20)
+    rew, done, dig, states, cnt = OP.trajectories(roms, ids, 4, acts, cfg=cfg, reset_seed=1, checkpoints={8})
+    for t in range(T):
+        assert (rew[t] == ref[t][1][ids]).all() and (done[t] == ref[t][2][ids]).all()
+        assert (dig[t] == OP.digest_rows(ref[t][0][ids])).all()
+    assert (states[8] == st8[ids]).all()
+    steps, final = OP.windows(roms, ids, 4, st8[ids], acts[8:, ids], cfg=cfg, reset_seed=1)
+    for k, (dg, r, d) in enumerate(steps):
+        assert (dg == OP.digest_rows(ref[8 + k][0][ids])).all() and (r == ref[8 + k][1][ids]).all()
+    assert (final == full.get_state()[ids]).all()
+    assert done.sum() > 0
