@@ -71,6 +71,15 @@ def parse():
     ap.add_argument("--idle-skip", type=int, default=0, choices=[0, 1],
                     help="exact idle-loop skip (off for the headline, SURVEY.md §7c.8)")
     ap.add_argument("--no-variant", action="store_true", help="skip the idle-skip-on variant run")
+    ap.add_argument("--sweep", type=int, default=1, choices=[0, 1],
+                    help="FPS vs num_envs sweep on R1 and on the cfg4 mix (rank 0, N=1 only)")
+    ap.add_argument("--sweep-envs", default="256,1024,4096,8192,16384,32768,65536")
+    ap.add_argument("--sweep-steps", type=int, default=60)
+    ap.add_argument("--sweep-warmup", type=int, default=100)
+    ap.add_argument("--e4", type=int, default=1, choices=[0, 1],
+                    help="E4 decorrelation diagnostic (PAPER.md P:452-465; rank 0, N=1 only)")
+    ap.add_argument("--window", type=int, default=100,
+                    help="counter all-reduce window in steps (SURVEY.md §8(e)), on a side stream")
     return ap.parse_args()
 
 
@@ -327,6 +336,119 @@ def run_vtrace(dev, pk):
     return out
 
 
+def time_steps(env, acts, t0, K, stream):
+    """Device time (ms) of K steps acts[t0:t0+K] on `stream` (CUDA events, sync on both sides)."""
+    import torch
+    torch.cuda.synchronize(env.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for t in range(t0, t0 + K):
+        env.step(acts[t])
+    e1.record(stream)
+    torch.cuda.synchronize(env.device)
+    return e0.elapsed_time(e1)
+
+
+def run_sweep(dev, args, stream):
+    """Emulated FPS vs num_envs (BASELINE.json metric "... vs num_envs"; SURVEY.md §8(d) sweep):
+    R1 alone and the cfg4 mix (R1-R4 interleaved), fs=4, GRAY84, random actions; each point
+    warms up `sweep_warmup` steps and times `sweep_steps`; the engine the library chose is named."""
+    import torch
+
+    from paper_1907_08467_b200 import Env
+    from paper_1907_08467_b200.inputs import games
+    out = {"steps": args.sweep_steps, "warmup": args.sweep_warmup, "fs": 4, "obs": "gray84", "points": {}}
+    W, K = args.sweep_warmup, args.sweep_steps
+    for label, names in (("R1", ["R1"]), ("cfg4_mix", ["R1", "R2", "R3", "R4"])):
+        roms = [games.build_rom(n) for n in names]
+        pts = []
+        for n in [int(x) for x in args.sweep_envs.split(",") if x]:
+            env = Env(roms, n, 4, device=dev)
+            env.reset(0)
+            gen = torch.Generator(device=dev)
+            gen.manual_seed(99)
+            acts = torch.randint(0, 18, (W + K, n), generator=gen, device=dev, dtype=torch.uint8)
+            for t in range(W):
+                env.step(acts[t])
+            ms = time_steps(env, acts, W, K, stream)
+            pts.append({"envs": n, "fps": n * 4 * K / (ms / 1000.0), "ms_per_step": ms / K, "engine": env.engine})
+            env.close()
+            del acts
+        out["points"][label] = pts
+    return out
+
+
+def run_e4(dev, stream, n_list=(512, 32768), steps=300, window=10):
+    """E4 decorrelation diagnostic: every env starts from ONE
+    cache entry (cule_set_state), random actions; FPS per 10-step window and the resets in each
+    window.  Identical envs start converged (no divergence) and decorrelate as random actions and
+    resets spread them, which is what the W = 200 warm-up of the bench skips."""
+    import numpy as np
+    import torch
+
+    from paper_1907_08467_b200 import Env
+    from paper_1907_08467_b200.inputs import games
+    rom = games.build_rom("R1")
+    out = {"rom": "R1", "fs": 4, "obs": "gray84", "window_steps": window, "runs": {}}
+    for n in n_list:
+        env = Env([rom], n, 4, device=dev)
+        env.reset(0)
+        st = env.get_state()
+        machine = np.r_[0:61, 64:192]
+        st[:, machine] = st[0, machine]          # every env = env 0's cache entry (same ROM)
+        env.set_state(st)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(5)
+        acts = torch.randint(0, 18, (steps, n), generator=gen, device=dev, dtype=torch.uint8)
+        fps, resets = [], []
+        for w0 in range(0, steps, window):
+            done_sum = torch.zeros((), dtype=torch.int64, device=dev)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t in range(w0, w0 + window):
+                _, _, d = env.step(acts[t])
+                done_sum += d.sum()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1)
+            fps.append(n * 4 * window / (ms / 1000.0))
+            resets.append(int(done_sum.item()))
+        out["runs"][str(n)] = {"engine": env.engine, "fps_per_window": fps, "resets_per_window": resets,
+                               "first_window_fps": fps[0], "last_10_windows_mean_fps": sum(fps[-10:]) / 10}
+        env.close()
+    out["note"] = ("the done-count reduction (torch) runs inside each window; it is the same for every window")
+    return out
+
+
+def oracle_single_core(rom_names, fs, mode):
+    """SURVEY.md §8(d) oracle baseline: FPS_1 = the oracle on ONE core (R1, fs=4, GRAY84, 64 envs
+    x 50 steps) and the cfg1 oracle wall time (16 envs x 100 frames, fs=1, RAW)."""
+    import numpy as np
+    import oracle
+    from paper_1907_08467_b200.inputs import games, palette
+    rom = games.build_rom("R1")
+    pal = palette.load_palette()
+    env = oracle.OracleEnv([rom], 64, 4, pal, obs_mode=1)
+    env.reset(0)
+    rng = np.random.default_rng(1234)
+    t0 = time.perf_counter()
+    for _ in range(50):
+        env.step(rng.integers(0, 18, 64, dtype=np.uint8))
+    dt = time.perf_counter() - t0
+    env.close()
+    t1 = time.perf_counter()
+    env = oracle.OracleEnv([rom], 16, 1, pal, obs_mode=0)
+    env.reset(0)
+    for _ in range(100):
+        env.step(rng.integers(0, 18, 16, dtype=np.uint8))
+    cfg1_wall = time.perf_counter() - t1
+    env.close()
+    return {"fps_1core": 64 * 4 * 50 / dt, "fps_1core_sample": "R1, fs=4, GRAY84, 64 envs x 50 steps, 1 process",
+            "cfg1_oracle_wall_s": cfg1_wall,
+            "cfg1_sample": "16 envs x 100 frames, fs=1, RAW (reset-cache build included)"}
+
+
 def run_cule(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -335,7 +457,10 @@ def run_cule(args, rank, world, local_rank):
     from paper_1907_08467_b200 import dist as D
     from paper_1907_08467_b200.inputs import games
 
-    build.build()
+    if local_rank == 0:
+        build.build()          # one build per node, before any rank loads the library
+    if world > 1:
+        dist.barrier()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     rom_names, envs, fs, mode, desc = CONFIGS[args.config]
@@ -362,14 +487,34 @@ def run_cule(args, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    # once per reporting window the int64[4] counters are copied on the step
+    # stream and all-reduced (NCCL, N > 1) on a side stream that waits only for that copy, so the
+    # collective never blocks the step stream
+    side = torch.cuda.Stream(dev)
+    win_bufs, win_works = [], []
     ev0.record(stream)
     for t in range(W, W + K):
         env.step(acts[t])
+        if args.window > 0 and (t - W + 1) % args.window == 0:
+            buf = torch.empty(4, dtype=torch.int64, device=dev)
+            env.counters_into(buf)
+            ready = torch.cuda.Event()
+            ready.record(stream)
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                buf.record_stream(side)
+                if world > 1:
+                    win_works.append(dist.all_reduce(buf, op=dist.ReduceOp.SUM, async_op=True))
+            win_bufs.append(buf)
     ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    for w in win_works:
+        w.wait()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    windows = [[int(x) for x in b.cpu().tolist()] for b in win_bufs]
     ms = ev0.elapsed_time(ev1)
     ms_max = D.max_over_ranks(ms, device=dev)
     counters = D.reduce_counters(env.counters())
@@ -473,9 +618,16 @@ def run_cule(args, rank, world, local_rank):
         "clocks": clk,
         "counters": {"frames": int(counters[0]), "episodes": int(counters[1]),
                      "return_sum": int(counters[2]), "faults": int(counters[3])},
+        "counter_windows": {"every_steps": args.window, "reduced_over_ranks": world > 1,
+                            "side_stream": True, "cumulative": windows},
     }
     if args.vtrace:
         line["vtrace"] = run_vtrace(dev, pk)
+    env.close()
+    if args.sweep and world == 1 and not args.envs:
+        line["sweep"] = run_sweep(dev, args, stream)
+    if args.e4 and world == 1 and not args.envs:
+        line["e4"] = run_e4(dev, stream)
     if not args.no_cpu_baseline and world == 1:
         cores = host_cores()
         procs = max(1, min(cores, 64))
@@ -485,6 +637,7 @@ def run_cule(args, rank, world, local_rank):
                                 "sample": f"{procs} processes x {args.cpu_sample_envs} envs x "
                                           f"{args.cpu_sample_steps} steps of {desc} ({frames} frames, "
                                           f"{t:.1f} s)", "cpu": cpu_model()}
+        line["cpu_baseline"].update(oracle_single_core(rom_names, fs, mode))
     print(json.dumps(line), flush=True)
 
 
@@ -501,8 +654,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # NCCL's INIT lines (ranks, communicator) stay visible on stderr for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_cule(args, rank, world, local_rank)
     finally:

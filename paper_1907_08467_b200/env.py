@@ -171,6 +171,14 @@ class Env:
                                              ctypes.c_void_p(self._sp(stream))))
         return self._counters
 
+    def counters_into(self, out: torch.Tensor, stream=None) -> torch.Tensor:
+        """Like counters(), into a caller-owned int64[4] device tensor (stream-ordered copy)."""
+        if out.dtype != torch.int64 or out.device != self.device or out.numel() != 4 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous int64[4] tensor on the env's device")
+        _lib.check(_lib.load().cule_counters(self._h, ctypes.c_void_p(out.data_ptr()),
+                                             ctypes.c_void_p(self._sp(stream))))
+        return out
+
     def debug_exec(self, n_instr: int, stream=None) -> torch.Tensor:
         status = torch.zeros(self.num_envs, dtype=torch.int32, device=self.device)
         _lib.check(_lib.load().cule_debug_exec(self._h, n_instr, ctypes.c_void_p(status.data_ptr()),
