@@ -76,7 +76,21 @@ typedef struct {
   int64_t env_index_base;     /* global id of local env 0 (multi-GPU sharding)               */
   const uint8_t* palette_rgb; /* HOST, 128 x (R,G,B) NTSC palette; read only during
                                  cule_create; required for GRAY84 (gray LUT), ignored for RAW  */
+  int32_t engine;             /* CULE_ENGINE_AUTO (default) or one of the engines below; the
+                                 environment variable CULE_ENGINE (simt|scalar|jit) overrides   */
 } cule_config;
+
+/* Engines (all compute the same results, bit for bit):
+ *   SIMT   batched datapath, up to 32 envs per warp;
+ *   SCALAR one env per warp, record-driven interpreter + warp-cooperative TIA replay;
+ *   JIT    the scalar engine with the cartridge code translated to CUDA at cule_create and
+ *          compiled with NVRTC for sm_100a (static recompilation; cached on disk by content).
+ * AUTO picks JIT where it applies (idle_skip off, the translation fits), else SCALAR up to
+ * 16384 envs, else SIMT. */
+#define CULE_ENGINE_AUTO 0
+#define CULE_ENGINE_SIMT 1
+#define CULE_ENGINE_SCALAR 2
+#define CULE_ENGINE_JIT 3
 
 /* Fill *cfg with the defaults above (score $80/$81, terminal $82 bit 0, seed 0, base 0). */
 void cule_default_config(cule_config* cfg);
@@ -161,11 +175,18 @@ int cule_debug_exec(cule_env* env, int n_instr, int32_t* d_status, void* cuda_st
 
 /* Number of envs / frameskip / observation bytes per env of a handle. */
 int cule_num_envs(const cule_env* env);
-/* Which step kernel the handle runs: 0 = batched SIMT engine (a few envs per warp, shared
- * micro-coded datapath), 1 = scalar engine (one env per warp, pre-decoded cartridge records).
- * Both implement the same machine model; chosen at create from the env count (CULE_ENGINE =
- * simt | scalar overrides).  CULE_E_CLOSED for a destroyed handle. */
+/* Which step kernel the handle runs: CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR or CULE_ENGINE_JIT
+ * (see cule_config.engine).  CULE_E_CLOSED for a destroyed handle. */
 int cule_engine(const cule_env* env);
+
+/* Host only (no GPU needed): translate the ROM set (as cule_create would for the JIT engine)
+ * and compile it with NVRTC for sm_100a into the on-disk kernel cache (directory jit_cache/
+ * next to libcule.so, or $CULE_JIT_CACHE), so a later cule_create finds it.  obs_mode selects
+ * the RAW or GRAY84 kernel.  `info` (may be NULL) receives a one-line summary.  Errors:
+ * CULE_E_INVAL, CULE_E_ROM_SIZE, CULE_E_CUDA (translation or compilation failed; message in
+ * cule_last_error). */
+int cule_jit_prepare(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int obs_mode, char* info,
+                     size_t info_len);
 int cule_frameskip(const cule_env* env);
 size_t cule_obs_bytes(const cule_env* env);
 

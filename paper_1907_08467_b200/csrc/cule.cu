@@ -20,6 +20,7 @@
 #include "scalar_predecode.h"
 #include "scalar_kernels.cuh"
 #include "vtrace.cuh"
+#include "jit.h"
 
 namespace {
 
@@ -72,6 +73,66 @@ bool compute_layout(int N, int n_roms, const cule_config* c, Layout* L) {
   return true;
 }
 
+// ROM images packed in 4 KB banks (a 2K cartridge stored twice: its mirror in the window),
+// per-ROM offsets and bank counts, and the scalar engine's pre-decoded records
+struct RomSet {
+  std::vector<uint8_t> img;
+  uint32_t rom_off[4] = {0, 0, 0, 0};
+  uint32_t banks[4] = {0, 0, 0, 0};
+  uint32_t rom_banks = 0;
+  uint32_t bytes = 0;
+  std::vector<uint64_t> recs;
+};
+
+int check_roms(const uint8_t* const* roms, const size_t* rom_lens, int n_roms) {
+  if (!roms || !rom_lens) return fail(CULE_E_INVAL, "null argument");
+  if (n_roms < 1 || n_roms > 4) return fail(CULE_E_INVAL, "n_roms must be in [1, 4]");
+  for (int r = 0; r < n_roms; ++r) {
+    if (!roms[r]) return fail(CULE_E_INVAL, "null ROM");
+    const size_t n = rom_lens[r];
+    if (n != 2048 && n != 4096 && n != 8192 && n != 16384 && n != 32768)
+      return fail(CULE_E_ROM_SIZE, "ROM size must be 2048 (2K), 4096 (4K), 8192 (F8), 16384 (F6) or 32768 (F4), got " +
+                                       std::to_string(n));
+  }
+  return CULE_OK;
+}
+
+RomSet make_romset(const uint8_t* const* roms, const size_t* rom_lens, int n_roms) {
+  RomSet rs;
+  uint32_t off = 0;
+  for (int r = 0; r < n_roms; ++r) {
+    rs.rom_off[r] = off;
+    const uint32_t img = rom_lens[r] < 4096 ? 4096u : (uint32_t)rom_lens[r];
+    off += img;
+    rs.banks[r] = img / 4096u;
+    rs.rom_banks |= (img / 4096u) << (8 * r);
+  }
+  rs.bytes = off;
+  rs.img.assign(off, 0);
+  for (int r = 0; r < n_roms; ++r) {
+    std::memcpy(rs.img.data() + rs.rom_off[r], roms[r], rom_lens[r]);
+    if (rom_lens[r] == 2048) std::memcpy(rs.img.data() + rs.rom_off[r] + 2048, roms[r], 2048);  // 2K mirror
+  }
+  rs.recs.resize(off);
+  uint32_t lens[4] = {0, 0, 0, 0};
+  for (int r = 0; r < n_roms; ++r) lens[r] = 4096u * rs.banks[r];
+  cule::predecode_roms(rs.img.data(), rs.rom_off, lens, n_roms, rs.recs.data());
+  return rs;
+}
+
+// translate + compile (or fetch from the caches) the JIT step kernel for a ROM set
+std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, size_t* n_insn, double* secs, bool* from_disk,
+                            std::string& err) {
+  cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
+  cule::jit::Translation t = tr.run(gray);
+  if (!t.ok) { err = t.why; return {}; }
+  *n_insn = t.n_insn;
+  if (const char* dump = getenv("CULE_JIT_DUMP")) {
+    if (FILE* f = fopen(dump, "w")) { fwrite(t.source.data(), 1, t.source.size(), f); fclose(f); }
+  }
+  return cule::jit::cubin_for(t.source, err, secs, from_disk);
+}
+
 }  // namespace
 
 struct cule_env {
@@ -92,6 +153,12 @@ struct cule_env {
   uint32_t sgrid;          // scalar engine: persistent blocks (<= one per SM)
   uint32_t slot_start[4], first_env[4];
   uint32_t grid;           // blocks of the step / debug kernels
+  bool jit = false;        // engine 1 runs the translated step kernel (jit.h)
+  CUmodule jit_mod = nullptr;
+  CUfunction jit_fn = nullptr;
+  size_t jit_smem = 0;     // dynamic shared memory of the translated kernel (no records staged)
+  size_t jit_insn = 0;
+  double jit_compile_s = 0.0;
 };
 
 static cule::Params base_params(const cule_env* e) {
@@ -183,11 +250,16 @@ static int sm_count() {
 // wins at low env counts (the batched engine is latency-bound there: a few envs per SM
 // sub-partition), the batched engine (SIMT datapath, issue-efficient) at high ones.  CULE_ENGINE
 // overrides (simt | scalar).
-static int choose_engine(int N) {
+static int requested_engine(const cule_config* c) {
   if (const char* v = getenv("CULE_ENGINE")) {
-    if (!strcmp(v, "simt")) return 0;
-    if (!strcmp(v, "scalar")) return 1;
+    if (!strcmp(v, "simt")) return CULE_ENGINE_SIMT;
+    if (!strcmp(v, "scalar")) return CULE_ENGINE_SCALAR;
+    if (!strcmp(v, "jit")) return CULE_ENGINE_JIT;
   }
+  return c->engine;
+}
+
+static int choose_engine(int N) {
   // measured (profiles/r01_v6_engine_sweep.txt): 4096 envs scalar 2.81M vs SIMT 0.74M FPS;
   // 16384 (F8) 2.72M vs 2.30M; 32768 (4 ROMs) 2.09M vs 2.87M
   return N <= 16384 ? 1 : 0;
@@ -239,6 +311,7 @@ void cule_default_config(cule_config* c) {
   c->env_index_base = 0;
   c->idle_skip = 0;
   c->palette_rgb = nullptr;
+  c->engine = CULE_ENGINE_AUTO;
 }
 
 size_t cule_workspace_bytes(int num_envs, int n_roms, const cule_config* cfg) {
@@ -268,6 +341,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   if (cfg->obs_mode == CULE_OBS_GRAY84 && !cfg->palette_rgb)
     return fail(CULE_E_INVAL, "GRAY84 needs cfg->palette_rgb (384 bytes)");
   if (((uintptr_t)d_workspace & 255) != 0) return fail(CULE_E_INVAL, "workspace must be 256-byte aligned");
+  if (cfg->engine < CULE_ENGINE_AUTO || cfg->engine > CULE_ENGINE_JIT) return fail(CULE_E_INVAL, "bad engine");
   for (int r = 0; r < n_roms; ++r) {
     if (!roms[r]) return fail(CULE_E_INVAL, "null ROM");
     const size_t n = rom_lens[r];
@@ -302,7 +376,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   }
   e->rom_bytes = off;
   e->epw = choose_epw(num_envs);
-  e->engine = choose_engine(num_envs);
+  const int want = requested_engine(cfg);
+  e->engine = want == CULE_ENGINE_SIMT ? 0 : (want == CULE_ENGINE_AUTO ? choose_engine(num_envs) : 1);
   {
     // records cost 8 B per ROM byte of shared memory: they fit for every combination up to
     // 4 x 4 KB or 2 x F8 + 1 x 4 KB (CULE_NO_REC=1 pretends they do not)
@@ -312,7 +387,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     if (optin <= 0) optin = 232448;
     const char* nr = getenv("CULE_NO_REC");
     e->use_rec = (!(nr && atoi(nr) == 1) && cule::scalar_smem_bytes(e->rom_bytes, true) <= (size_t)optin) ? 1u : 0u;
-    if (!e->use_rec) e->engine = 0;  // the scalar engine runs from the records: batched engine otherwise
+    if (!e->use_rec && want != CULE_ENGINE_JIT) e->engine = 0;  // the interpreter runs from the records
+    e->jit_smem = cule::scalar_smem_bytes(e->rom_bytes, false);
     e->ssmem = cule::scalar_smem_bytes(e->rom_bytes, e->use_rec != 0u);
     const uint32_t need = ((uint32_t)num_envs + cule::kSWarps - 1) / cule::kSWarps;
     const uint32_t sms = (uint32_t)sm_count();
@@ -402,6 +478,38 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     delete e;
     return fail(CULE_E_ROM_FAULT, "reset-cache build hit a JAM or runaway frame");
   }
+  // the translated engine: explicitly requested, or AUTO where it applies (idle skip off)
+  if (want == CULE_ENGINE_JIT || (want == CULE_ENGINE_AUTO && !cfg->idle_skip)) {
+    std::string jerr;
+    bool from_disk = false;
+    std::vector<char> cubin;
+    auto& drv = cule::jit::driver();
+    if (!drv.ok) jerr = "CUDA driver entry points unavailable";
+    else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
+    else {
+      RomSet rs = make_romset(roms, rom_lens, n_roms);
+      cubin = jit_cubin(rs, n_roms, g, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+    }
+    CUresult cr = CUDA_SUCCESS;
+    if (!cubin.empty()) {
+      cr = drv.moduleLoadData(&e->jit_mod, cubin.data());
+      if (cr == CUDA_SUCCESS) cr = drv.moduleGetFunction(&e->jit_fn, e->jit_mod, "cule_jit_step");
+      if (cr == CUDA_SUCCESS)
+        cr = drv.funcSetAttribute(e->jit_fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)e->jit_smem);
+      if (cr != CUDA_SUCCESS) jerr = "loading the translated kernel failed (CUresult " + std::to_string((int)cr) + ")";
+    }
+    if (jerr.empty() && e->jit_fn) {
+      e->jit = true;
+      e->engine = 1;
+    } else if (want == CULE_ENGINE_JIT) {
+      if (e->jit_mod) drv.moduleUnload(e->jit_mod);
+      delete e;
+      return fail(CULE_E_CUDA, "JIT engine: " + jerr);
+    } else if (e->jit_mod) {
+      drv.moduleUnload(e->jit_mod);
+      e->jit_mod = nullptr;
+    }
+  }
   {
     std::lock_guard<std::mutex> lk(g_live_mu);
     g_live.insert(e);
@@ -453,6 +561,14 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
     // the persistent kernel's work tickets start from zero on the launch stream (the kernel also
     // re-zeroes them when it finishes; this covers an aborted launch)
     cudaMemsetAsync(e->ws + e->L.tickets, 0, 16, s);
+    if (e->jit) {
+      p.use_rec = 0u;  // the translated kernel stages no records
+      void* args[] = {&p};
+      const CUresult cr = cule::jit::driver().launchKernel(e->jit_fn, sg, 1, 1, 32 * cule::kSWarps, 1, 1,
+                                                           (unsigned)e->jit_smem, (CUstream)s, args, nullptr);
+      if (cr != CUDA_SUCCESS) return fail(CULE_E_CUDA, "cule_jit_step launch failed (CUresult " + std::to_string((int)cr) + ")");
+      return cuda_check("cule_jit_step");
+    }
     if (e->cfg.obs_mode == CULE_OBS_GRAY84) cule::scalar_kernel<true, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
     else cule::scalar_kernel<false, false><<<sg, 32 * cule::kSWarps, e->ssmem, s>>>(p);
   } else if (e->cfg.obs_mode == CULE_OBS_GRAY84) {
@@ -558,7 +674,7 @@ int cule_debug_exec(cule_env* e, int n_instr, int32_t* d_status, void* stream) {
   cule::Params p = base_params(e);
   p.debug_instr = n_instr;
   p.debug_status = d_status;
-  if (e->engine == 1) {
+  if (e->engine == 1 && e->use_rec) {  // the translated engine has no debug entry: the interpreter's
     const uint32_t sg = e->sgrid;
     cudaMemsetAsync(e->ws + e->L.tickets, 0, 16, static_cast<cudaStream_t>(stream));
     cule::scalar_kernel<false, true><<<sg, 32 * cule::kSWarps, e->ssmem, static_cast<cudaStream_t>(stream)>>>(p);
@@ -587,7 +703,29 @@ int cule_vtrace(const float* d_rewards, const float* d_values, const float* d_bo
 
 int cule_num_envs(const cule_env* e) { return live(e) ? e->N : CULE_E_CLOSED; }
 int cule_frameskip(const cule_env* e) { return live(e) ? e->fs : CULE_E_CLOSED; }
-int cule_engine(const cule_env* e) { return live(e) ? e->engine : CULE_E_CLOSED; }
+int cule_engine(const cule_env* e) {
+  if (!live(e)) return CULE_E_CLOSED;
+  return e->engine == 0 ? CULE_ENGINE_SIMT : (e->jit ? CULE_ENGINE_JIT : CULE_ENGINE_SCALAR);
+}
+
+int cule_jit_prepare(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int obs_mode, char* info,
+                     size_t info_len) {
+  int rc = check_roms(roms, rom_lens, n_roms);
+  if (rc) return rc;
+  if (obs_mode != CULE_OBS_RAW && obs_mode != CULE_OBS_GRAY84) return fail(CULE_E_INVAL, "bad obs_mode");
+  RomSet rs = make_romset(roms, rom_lens, n_roms);
+  size_t n_insn = 0;
+  double secs = 0.0;
+  bool from_disk = false;
+  std::string err;
+  std::vector<char> cubin = jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, &n_insn, &secs, &from_disk, err);
+  if (cubin.empty()) return fail(CULE_E_CUDA, "JIT: " + err);
+  if (info && info_len) {
+    snprintf(info, info_len, "%zu instructions translated, cubin %zu bytes, %s %.1f s, cache %s", n_insn,
+             cubin.size(), from_disk ? "loaded from disk" : "compiled in", secs, cule::jit::cache_dir().c_str());
+  }
+  return CULE_OK;
+}
 size_t cule_obs_bytes(const cule_env* e) { return live(e) ? obs_bytes_of(e->cfg.obs_mode) : 0; }
 
 int cule_destroy(cule_env* e) {
@@ -596,6 +734,7 @@ int cule_destroy(cule_env* e) {
     if (!e || !g_live.count(e)) return fail(CULE_E_CLOSED, "invalid or destroyed cule_env handle");
     g_live.erase(e);
   }
+  if (e->jit_mod) cule::jit::driver().moduleUnload(e->jit_mod);
   delete e;
   return CULE_OK;
 }

@@ -16,8 +16,10 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef __CUDACC_RTC__  // host-only table builders (not compiled by NVRTC, jit.h)
 #include <initializer_list>
 #include <utility>
+#endif
 
 namespace cule {
 
@@ -138,6 +140,7 @@ inline uint64_t entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr, c
   return (uint64_t)lo | ((uint64_t)u.hi << 32);
 }
 
+#ifndef __CUDACC_RTC__
 inline void build_decode_table(uint64_t* table) {
   using namespace dk;
   Micro nop;
@@ -250,5 +253,6 @@ inline void build_decode_table(uint64_t* table) {
   spc(0x6B, AM_IMM, 2, SP_ARR);
   spc(0xCB, AM_IMM, 2, SP_SBX);
 }
+#endif  // __CUDACC_RTC__
 
 }  // namespace cule

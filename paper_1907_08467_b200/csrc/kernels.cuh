@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(128, CULE_MINB) step_kernel(Params p) {
   }
 }
 
+#ifndef CULE_JIT  // the jit module (jit.h) holds only the translated step kernel
 // ---- debug: n instructions per env, no rendering ------------------------------------------------
 __global__ void __launch_bounds__(128) debug_kernel(Params p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -625,5 +626,7 @@ __global__ void unpack_kernel(uint8_t* state, const uint8_t* packed, uint32_t N)
   if (k >= 13) v = make_uint4(0, 0, 0, 0); // bytes 208-255 reserved
   reinterpret_cast<uint4*>(state)[k * N + i] = v;
 }
+
+#endif  // CULE_JIT
 
 }  // namespace cule

@@ -14,8 +14,10 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef __CUDACC_RTC__  // host-only table builders (not compiled by NVRTC, jit.h)
 #include <initializer_list>
 #include <utility>
+#endif
 
 #include "decode_table.h"
 
@@ -78,6 +80,7 @@ inline uint64_t s_entry(uint32_t mode, uint32_t cyc, bool pen, bool rd, bool wr,
   return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
+#ifndef __CUDACC_RTC__
 inline void build_scalar_table(uint64_t* t) {
   // JAM and the unstable opcodes: 1-byte fetch, 0 cycles, fault (DESIGN.md §2 R#1)
   for (int i = 0; i < 256; i++) t[i] = s_entry(AM_IMP, 0, false, false, false, K_JAM, 0);
@@ -169,5 +172,6 @@ inline void build_scalar_table(uint64_t* t) {
   t[0x6B] = s_entry(AM_IMM, 2, false, false, false, K_ARR, 0);
   t[0xCB] = s_entry(AM_IMM, 2, false, false, false, K_SBX, 0);
 }
+#endif  // __CUDACC_RTC__
 
 }  // namespace cule

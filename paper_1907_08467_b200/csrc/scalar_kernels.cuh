@@ -168,9 +168,16 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
   for (;;) {
     uint32_t ev = SE_NONE;
     if (lane == 0u) {
+#ifdef CULE_JIT
+      // the translated engine (jit.h): the ROMs' code compiled into run_cpu_jit (no debug entry)
+      ev = run_cpu_jit(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles);
+      (void)budget;
+      (void)rec_s;
+#else
       ev = (!kDebug && M->idle_skip)
                ? run_cpu<kDebug, !kDebug>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget, rec_s)
                : run_cpu<kDebug, false>(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles, budget, rec_s);
+#endif
     }
     ev = __shfl_sync(kFull, ev, 0);
     __syncwarp();
@@ -341,7 +348,7 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
 // envs of different lengths balance across the SMs and the staged ROM/record images are reused.
 // The last warp to finish resets the counters for the next launch on the stream.
 template <bool kGray, bool kDebug>
-__global__ void __launch_bounds__(32 * kSWarps, 1) scalar_kernel(Params p) {
+__device__ __forceinline__ void scalar_kernel_body(const Params& p) {
   extern __shared__ __align__(16) uint8_t smem[];
   stage_block_s(p, smem);
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
@@ -363,5 +370,12 @@ __global__ void __launch_bounds__(32 * kSWarps, 1) scalar_kernel(Params p) {
     }
   }
 }
+
+#ifndef CULE_JIT
+template <bool kGray, bool kDebug>
+__global__ void __launch_bounds__(32 * kSWarps, 1) scalar_kernel(Params p) {
+  scalar_kernel_body<kGray, kDebug>(p);
+}
+#endif
 
 }  // namespace cule

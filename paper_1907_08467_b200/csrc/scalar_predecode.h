@@ -73,6 +73,7 @@ constexpr uint32_t C_HOT_LAST = C_WSYNC;
 
 constexpr uint32_t kRecBytes = 8;
 
+#ifndef __CUDACC_RTC__  // host only (the jit compiles the device headers with NVRTC)
 // decode the record for an instruction starting at bank offset o of a 4 KB bank image
 inline uint64_t predecode_one(const uint8_t* bank, uint32_t o, uint32_t nbanks, const uint64_t* stab) {
   // hotspots of the bank-switching scheme: window offsets [hs, hs + nbanks) (F8 $FF8, F6 $FF6,
@@ -209,5 +210,7 @@ inline void predecode_roms(const uint8_t* img, const uint32_t* rom_off, const ui
     }
   }
 }
+
+#endif  // __CUDACC_RTC__
 
 }  // namespace cule

@@ -43,6 +43,11 @@ class Env:
         c.seed = seed
         c.env_index_base = env_index_base
         fields = {f for f, _ in _lib.CuleConfig._fields_} - {"obs_mode", "palette_rgb"}
+        if isinstance(cfg.get("engine"), str):
+            names = {v: k for k, v in _lib.ENGINE_NAMES.items()} | {"auto": _lib.CULE_ENGINE_AUTO}
+            if cfg["engine"] not in names:
+                raise ValueError(f"engine must be one of {sorted(names)}")
+            cfg["engine"] = names[cfg["engine"]]
         for k, v in cfg.items():
             if k not in fields:
                 raise ValueError(f"unknown config key {k!r}; valid keys: {sorted(fields)}")
@@ -74,7 +79,7 @@ class Env:
             self.dones = torch.zeros(self.num_envs, dtype=torch.uint8, device=self.device)
             self._counters = torch.zeros(4, dtype=torch.int64, device=self.device)
         self.obs_bytes = int(np.prod(shape))
-        self.engine = "scalar" if _lib.check(L.cule_engine(self._h)) == 1 else "simt"
+        self.engine = _lib.ENGINE_NAMES[_lib.check(L.cule_engine(self._h))]
 
     def _sp(self, stream) -> int:
         """The caller's stream, else the current stream of the env's device (not of whatever

@@ -41,11 +41,13 @@ def _built():
 
 
 def gpu_run(roms, N, fs, acts, *, track=(), digest_all_steps=(), checkpoints=(), reset_seed=0, engine=None,
-            **cfg):
+            engine_cfg=None, **cfg):
     """One GPU run through the C-ABI: rewards/dones of every env and step, digests of the
     tracked envs every step (of all envs on digest_all_steps), full snapshots before the
     checkpoint steps."""
     from paper_1907_08467_b200 import Env
+    if engine_cfg is not None:
+        cfg["engine"] = engine_cfg
     env = Env(roms, N, fs, **cfg)
     if engine is not None:
         assert env.engine == engine, (env.engine, engine)
@@ -86,14 +88,14 @@ def check_full_size(roms, N, engine, base_set, n_resets, window_ids, T=310, wind
     fs = 4
     acts = H.random_actions(N, T, 1234)
     # pass 1: which envs reset first (rewards/dones of every env are compared in pass 2 as well)
-    p1 = gpu_run(roms, N, fs, acts, engine=engine)
+    p1 = gpu_run(roms, N, fs, acts, engine=engine, engine_cfg=engine)
     resets = first_resets(p1["done"], n_resets)
     assert len(resets) == n_resets, f"only {len(resets)} envs reset in {T} steps"
     track = np.union1d(base_set, resets)
     checkpoints = set(window_steps) | {s + W for s in window_steps} | {T}
     digest_all = {s + k for s in window_steps for k in range(W)}
     g = gpu_run(roms, N, fs, acts, track=track, digest_all_steps=digest_all, checkpoints=checkpoints,
-                engine=engine)
+                engine=engine, engine_cfg=engine)
     assert (g["rew"] == p1["rew"]).all() and (g["done"] == p1["done"]).all(), "GPU run not deterministic"
 
     # full trajectories of the tracked envs
@@ -123,18 +125,20 @@ def check_full_size(roms, N, engine, base_set, n_resets, window_ids, T=310, wind
     return len(track), n_done_tracked
 
 
-def test_cfg2_full_trajectory_and_windows():
+@pytest.mark.parametrize("engine", ["jit", "scalar"])
+def test_cfg2_full_trajectory_and_windows(engine):
     N = 4096
     base = np.union1d(np.arange(256), np.arange(0, N, 256))
-    n_track, n_done = check_full_size([games.build_rom("R1")], N, "scalar", base, 256, np.arange(N))
+    n_track, n_done = check_full_size([games.build_rom("R1")], N, engine, base, 256, np.arange(N))
     assert n_track >= len(base) + 200 and n_done >= 256   # the resets overlap the base set a little
 
 
-def test_cfg4_full_trajectory_and_windows():
+@pytest.mark.parametrize("engine", ["simt", "jit"])
+def test_cfg4_full_trajectory_and_windows(engine):
     N = 32768
     roms = [games.build_rom(n) for n in ("R1", "R2", "R3", "R4")]
     base = np.union1d(np.arange(128), np.arange(0, N, 64))
-    n_track, n_done = check_full_size(roms, N, "simt", base, 128, np.arange(0, N, 8))
+    n_track, n_done = check_full_size(roms, N, engine, base, 128, np.arange(0, N, 8))
     assert n_track >= len(base) + 64 and n_done >= 128
 
 

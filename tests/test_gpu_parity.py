@@ -14,12 +14,18 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.fixture(autouse=True, params=["simt", "scalar"])
+@pytest.fixture(autouse=True, params=["simt", "scalar", "jit"])
 def engine(request, monkeypatch):
-    """Every parity test runs on both engines: the batched SIMT datapath and the scalar engine
-    (one env per warp, compact interpreter, warp-cooperative TIA replay)."""
+    """Every parity test runs on all three engines: the batched SIMT datapath, the scalar engine
+    (one env per warp, record-driven interpreter, warp-cooperative TIA replay) and the JIT
+    engine (the scalar engine with the cartridge code translated to CUDA, csrc/jit.h)."""
     monkeypatch.setenv("CULE_ENGINE", request.param)
     return request.param
+
+
+def skip_jit_debug(engine):
+    if engine == "jit":
+        pytest.skip("debug-entry test: the JIT engine's debug_exec runs the scalar interpreter (tested as 'scalar')")
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -215,6 +221,7 @@ def test_random_instructions(n_instr, engine):
     windows, zero-page indexing into the TIA, RAM-based abs,Y page crosses, F8 hotspots, code
     in RAM) are all exercised.  Two 4 KB + one F8 ROM for the scalar engine (its records must fit
     in shared memory), two of each for the batched engine."""
+    skip_jit_debug(engine)
     import oracle
     from paper_1907_08467_b200 import Env
     rng = np.random.default_rng(100 + n_instr)
@@ -254,6 +261,7 @@ def test_mapper_random_instructions(n_instr, engine):
     $1FF6-$1FF9 and $1FF4-$1FFB, the 2K mirror) through the debug entry, against the oracle.
     The scalar engine takes 2K + F6 (its records must fit in shared memory); F4 runs on the
     batched engine."""
+    skip_jit_debug(engine)
     import oracle
     from paper_1907_08467_b200 import Env
     rng = np.random.default_rng(500 + n_instr)
@@ -282,6 +290,7 @@ def test_mapper_random_instructions(n_instr, engine):
 def test_m22_bank_programs(nbanks, engine):
     """The F6 / F4 micro-programs (oracle pins in test_oracle_riot_cart.py) give the same state
     on the GPU after every step of 37 instructions."""
+    skip_jit_debug(engine)
     import oracle
     from paper_1907_08467_b200 import Env
     if engine == "scalar" and nbanks == 8:
@@ -427,10 +436,12 @@ def test_frame_stack_parity(roms):
 
 
 @pytest.mark.parametrize("src", ["R1", "R2", "R4", "m20", "m21"])
-def test_idle_skip_is_exact(src):
+def test_idle_skip_is_exact(src, engine):
     """The exact idle-loop skip (cule_config.idle_skip; R#24) skips
     whole [timer read; branch back] poll iterations in closed form: observations, rewards,
     dones, counters and the full state stay bit-identical to the oracle, which never skips."""
+    if engine == "jit":
+        pytest.skip("the JIT engine has no idle-loop skip (cule_create rejects the combination)")
     import oracle
     from paper_1907_08467_b200 import Env
     rom = games.build_rom(src) if src.startswith("R") else micro.build(
