@@ -478,8 +478,12 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     delete e;
     return fail(CULE_E_ROM_FAULT, "reset-cache build hit a JAM or runaway frame");
   }
-  // the translated engine: explicitly requested, or AUTO where it applies (idle skip off)
-  if (want == CULE_ENGINE_JIT || (want == CULE_ENGINE_AUTO && !cfg->idle_skip)) {
+  // the translated engine: explicitly requested, or AUTO where it wins (measured sweep,
+  // profiles/r02_engine_sweep.txt: one ROM at every env count; mixed ROM sets up to 16384 envs —
+  // beyond that the batched engine amortises its datapath over 32 envs per warp and the
+  // translated code of several ROMs crowds the instruction cache) and applies (idle skip off)
+  const bool jit_auto = want == CULE_ENGINE_AUTO && !cfg->idle_skip && (n_roms == 1 || num_envs <= 16384);
+  if (want == CULE_ENGINE_JIT || jit_auto) {
     std::string jerr;
     bool from_disk = false;
     std::vector<char> cubin;

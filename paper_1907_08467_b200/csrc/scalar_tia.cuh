@@ -176,30 +176,43 @@ __device__ __forceinline__ uint32_t obj_word(uint32_t k, uint32_t pat, uint32_t 
 // coverage of the six objects in word k
 struct Words { uint32_t p0, p1, m0, m1, bl, pf; };
 
-__device__ __forceinline__ uint32_t player_word(uint32_t k, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl) {
-  if (g == 0u) return 0u;
-  const uint32_t mode = nusiz & 7u;
-  uint32_t pat = refl ? g : rev8(g);  // pixel d shows graphic bit 7-d (bit d when reflected)
-  if (mode == 5u) pat = spread2(pat);
-  else if (mode == 7u) pat = spread4(pat);
-  return obj_word(k, pat, pos, Tia::copies(mode));
-}
-__device__ __forceinline__ uint32_t missile_word(uint32_t k, uint32_t pos, uint32_t nusiz, bool en) {
-  if (!en) return 0u;
-  const uint32_t mode = nusiz & 7u;
-  const uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3u))) - 1u;
-  return obj_word(k, pat, pos, (mode == 5u || mode == 7u) ? 1u : Tia::copies(mode));
-}
-
 // coverage words of the six objects in the lane's word k, recomputed only for the objects
-// flagged in `dirty`; playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), 4 px each
+// flagged in `dirty`; playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), 4 px each.
+// One obj_word call site in a (warp-uniform) loop over the five movable objects keeps the hot
+// replay code small (the SM's instruction cache holds ~32 KB).
 __device__ __forceinline__ void update_words(const TiaP& t, uint32_t k, Words& w, uint32_t dirty) {
-  if (dirty & 1u) w.p0 = player_word(k, byte_of(t.w6, 0), byte_of(t.w2, 0), t.grp0(), t.f(1));
-  if (dirty & 2u) w.p1 = player_word(k, byte_of(t.w6, 1), byte_of(t.w2, 1), t.grp1(), t.f(2));
-  if (dirty & 4u) w.m0 = missile_word(k, byte_of(t.w6, 2), byte_of(t.w2, 0), t.f(3) && !t.f(10));
-  if (dirty & 8u) w.m1 = missile_word(k, byte_of(t.w6, 3), byte_of(t.w2, 1), t.f(4) && !t.f(11));
-  if (dirty & 16u)
-    w.bl = t.ball_on() ? obj_word(k, (1u << (1u << ((byte_of(t.w1, 3) >> 4) & 3u))) - 1u, byte_of(t.w7, 0), 1u) : 0u;
+  uint32_t todo = dirty & 31u;
+#pragma unroll 1
+  while (todo) {
+    const uint32_t o = (uint32_t)__ffs(todo) - 1u;
+    todo &= todo - 1u;
+    const uint32_t idx = o & 1u;                       // P0/M0: 0, P1/M1: 1
+    const uint32_t nusiz = byte_of(t.w2, (int)idx), mode = nusiz & 7u;
+    uint32_t pat, pos, cps;
+    if (o < 2u) {        // players: graphic (VDEL copy, reflection), scaled in modes 5/7
+      const uint32_t g = idx ? t.grp1() : t.grp0();
+      uint32_t q = t.f(1 + (int)idx) ? g : rev8(g);   // pixel d shows graphic bit 7-d (bit d reflected)
+      q = mode == 5u ? spread2(q) : (mode == 7u ? spread4(q) : q);
+      pat = g ? q : 0u;
+      pos = byte_of(t.w6, (int)idx);
+      cps = Tia::copies(mode);
+    } else if (o < 4u) { // missiles: enabled and not locked to the player; one copy in modes 5/7
+      const bool en = t.f(3 + (int)idx) && !t.f(10 + (int)idx);
+      pat = en ? (1u << (1u << ((nusiz >> 4) & 3u))) - 1u : 0u;
+      pos = byte_of(t.w6, 2 + (int)idx);
+      cps = (mode == 5u || mode == 7u) ? 1u : Tia::copies(mode);
+    } else {             // ball
+      pat = t.ball_on() ? (1u << (1u << ((byte_of(t.w1, 3) >> 4) & 3u))) - 1u : 0u;
+      pos = byte_of(t.w7, 0);
+      cps = 1u;
+    }
+    const uint32_t v = pat ? obj_word(k, pat, pos, cps) : 0u;
+    if (o == 0u) w.p0 = v;
+    else if (o == 1u) w.p1 = v;
+    else if (o == 2u) w.m0 = v;
+    else if (o == 3u) w.m1 = v;
+    else w.bl = v;
+  }
   if (dirty & 32u) {
     const uint32_t left = ((byte_of(t.w1, 0) >> 4) & 0xFu) | (rev8(byte_of(t.w1, 1)) << 4) | (byte_of(t.w1, 2) << 12);
     const uint32_t right = (t.w1 & 0x01000000u) ? (__brev(left) >> 12) : left;
@@ -254,7 +267,7 @@ __device__ __forceinline__ void shade_init(uint32_t shade_s, uint32_t w0, const 
 
 // output row i (0..83) of the exact area average from input rows r0, r0+1, r0+2 of the ring
 // (rows weighted 2:2:1 for even i, 1:2:2 for odd i; total weight 200, round half to even, R#17)
-__device__ __forceinline__ void area84_row(uint32_t ring_s, uint32_t cols_s, uint32_t r0, uint32_t i, uint8_t* out,
+__device__ __noinline__ void area84_row(uint32_t ring_s, uint32_t cols_s, uint32_t r0, uint32_t i, uint8_t* out,
                                            uint32_t lane) {
   const uint32_t q0 = ring_s + (r0 % 3u) * 160u;
   const uint32_t q1 = ring_s + ((r0 + 1u) % 3u) * 160u;
@@ -303,13 +316,18 @@ __device__ __forceinline__ void fused_row(const RowBuf& rb, uint32_t lane) {
   }
 }
 
-// collision bits of visible pixels [xa, xb) reduced over the warp (even lanes 0..8 hold word lane/2)
-__device__ __forceinline__ uint32_t collide_coop(const Words& w, uint32_t lane, uint32_t xa, uint32_t xb) {
+// collision bits of the visible pixels [a0, b0) U [a1, b1), reduced over the warp (even lanes
+// 0..8 hold 32-pixel word lane/2)
+__device__ __forceinline__ uint32_t range_bits(uint32_t lo, uint32_t xa, uint32_t xb) {
+  const uint32_t s = xa > lo ? min(xa - lo, 32u) : 0u, e = xb > lo ? min(xb - lo, 32u) : 0u;
+  return e > s ? ((e - s == 32u ? 0xFFFFFFFFu : ((1u << (e - s)) - 1u)) << s) : 0u;
+}
+__device__ __forceinline__ uint32_t collide_coop(const Words& w, uint32_t lane, uint32_t a0, uint32_t b0, uint32_t a1,
+                                                 uint32_t b1) {
   uint32_t bits = 0u;
   if (lane < 10u && !(lane & 1u)) {
     const uint32_t lo = 16u * lane;
-    const uint32_t s = xa > lo ? min(xa - lo, 32u) : 0u, e = xb > lo ? min(xb - lo, 32u) : 0u;
-    const uint32_t r = e > s ? ((e - s == 32u ? 0xFFFFFFFFu : ((1u << (e - s)) - 1u)) << s) : 0u;
+    const uint32_t r = range_bits(lo, a0, b0) | range_bits(lo, a1, b1);
     const uint32_t p0 = w.p0 & r, p1 = w.p1 & r, m0 = w.m0 & r, m1 = w.m1 & r, bl = w.bl & r, pf = w.pf & r;
     bits = ((m0 & p1) ? 1u : 0u) | ((m0 & p0) ? 2u : 0u) | ((m1 & p0) ? 4u : 0u) | ((m1 & p1) ? 8u : 0u) |
            ((p0 & pf) ? 0x10u : 0u) | ((p0 & bl) ? 0x20u : 0u) | ((p1 & pf) ? 0x40u : 0u) |
@@ -380,15 +398,10 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
     dirty = 0u;
   }
   if (need_coll) {  // collisions depend on x only: the union of the span's visible x ranges
-    uint32_t bits;
-    if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) {
-      bits = collide_coop(w, lane, 0u, 160u);
-    } else if (l1 == l0) {
-      bits = xb1 > xa0 ? collide_coop(w, lane, xa0, xb1) : 0u;
-    } else {
-      bits = (xa0 < 160u ? collide_coop(w, lane, xa0, 160u) : 0u) | (xb1 > 0u ? collide_coop(w, lane, 0u, xb1) : 0u);
-    }
-    t.w7 |= bits << 16;
+    uint32_t a0 = xa0, b0 = 160u, a1 = 0u, b1 = xb1;   // two partial lines (l1 == l0 + 1)
+    if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) { a0 = 0u; b1 = 0u; }  // every x
+    else if (l1 == l0) { b0 = xb1; b1 = 0u; }                                  // one line
+    t.w7 |= collide_coop(w, lane, a0, b0, a1, b1) << 16;
   }
   if (!any_win) return;
   uint32_t x0w = rb.fill, x1w = rb.fill, x2w = rb.fill, x3w = rb.fill;
@@ -422,10 +435,13 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
   t.load(tw);
   Words w{0u, 0u, 0u, 0u, 0u, 0u};
   uint32_t dirty = 0x3Fu;
-  for (uint32_t k = 0; k < n; ++k) {
-    const uint32_t e = lg[k];
+  // entries 0..n-1, then (fin) the final catch-up to t_final: one catch_up_coop call site
+  const uint32_t kend = fin ? n + 1u : n;
+  for (uint32_t k = 0; k < kend; ++k) {
+    const uint32_t e = k < n ? lg[k] : (t_final << 14);
     const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
     catch_up_coop(t, T, rb, lane, ystart, gray, w, dirty);
+    if (k == n) break;
     __syncwarp();  // reconverge: the register update is warp-uniform work, issued once
     t.apply(r, e & 0xFFu, T);
     if (r - 6u < 4u) {  // COLUxx: refresh the shaded colour, ordered before any lane's next read
@@ -434,7 +450,6 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
     }
     dirty |= kDirtyTable.v[r];
   }
-  if (fin) catch_up_coop(t, t_final, rb, lane, ystart, gray, w, dirty);
   __syncwarp();
   if (lane == 0u) t.store(tw);
   __syncwarp();
@@ -442,7 +457,7 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
 }
 
 // after the frame's last catch-up: store the partial row and black out the rows never reached
-__device__ __forceinline__ void finish_frame_coop(RowBuf& rb, uint32_t lane) {
+__device__ __noinline__ void finish_frame_coop(RowBuf& rb, uint32_t lane) {
   if (!rb.render) return;
   if (rb.obs84) {  // the partial row, then black rows, through the fused reduction
     while (rb.row < (uint32_t)kFrameH) row_done(rb, lane);
