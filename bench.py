@@ -586,14 +586,25 @@ def run_cule(args, rank, world, local_rank):
     issue = {"unit": "Twarp-inst/s", "peak": issue_peak,
              "achieved": (ipf * envs * fs / launch_s / 1e12) if ipf else None}
     issue["frac"] = issue["achieved"] / issue_peak if issue["achieved"] else None
+    # lane-level issue: thread-instructions per second against 32 lanes per issue slot
+    tpf = prof.get("thread_inst_per_frame") if prof else None
+    lane_peak = issue_peak * 32.0
+    lane = {"unit": "Tthread-inst/s", "peak": lane_peak,
+            "achieved": (tpf * envs * fs / launch_s / 1e12) if tpf else None,
+            "threads_per_warp_inst": prof.get("threads_per_inst") if prof else None}
+    lane["frac"] = lane["achieved"] / lane_peak if lane["achieved"] else None
     roof = {"bound": "alu", "unit": "Twarp-inst/s (integer ALU pipe)", "peak": alu_peak,
             "achieved": (apf * envs * fs / launch_s / 1e12) if apf else None,
             "issue": issue,
+            "lane_issue": lane,
             "traffic": prof["dram_bytes_per_launch"] if prof else None,
+            "traffic_over_algorithmic": (prof["dram_bytes_per_launch"] / alg_bytes) if prof else None,
             "profile": prof["source"] if prof else None,
             "alu_pipe_frac_ncu": prof.get("alu_pipe_frac") if prof else None,
             "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": pk["hbm_gbs"], "frac": hbm_gbs / pk["hbm_gbs"],
-                    "alg_bytes_per_launch": alg_bytes},
+                    "alg_bytes_per_launch": alg_bytes,
+                    "note": "north_star's HBM fraction for state-plus-frame traffic: algorithmic bytes "
+                            "(2x208 state + 6 action/reward/done + observation per env-step) / launch time"},
             "peak_source": pk["source"] + "; ALU and issue peaks from 148 SMs x 4 SMSPs x max SM clock"}
     roof["frac"] = roof["achieved"] / alu_peak if roof["achieved"] else None
     line = {
