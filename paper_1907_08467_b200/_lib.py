@@ -27,7 +27,7 @@ EXPORTS = ["cule_default_config", "cule_workspace_bytes", "cule_create", "cule_r
            "cule_step", "cule_step_host", "cule_get_state", "cule_set_state", "cule_counters",
            "cule_debug_exec", "cule_num_envs", "cule_frameskip", "cule_obs_bytes",
            "cule_engine", "cule_reset_stacked", "cule_step_stacked", "cule_vtrace", "cule_destroy", "cule_last_error",
-           "cule_jit_prepare"]
+           "cule_jit_prepare", "cule_jit_prepare_engine"]
 
 
 class CuleConfig(ctypes.Structure):
@@ -41,8 +41,9 @@ class CuleConfig(ctypes.Structure):
                 ("palette_rgb", ctypes.POINTER(ctypes.c_uint8)),
                 ("engine", ctypes.c_int32)]
 
-CULE_ENGINE_AUTO, CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR, CULE_ENGINE_JIT = 0, 1, 2, 3
-ENGINE_NAMES = {CULE_ENGINE_SIMT: "simt", CULE_ENGINE_SCALAR: "scalar", CULE_ENGINE_JIT: "jit"}
+CULE_ENGINE_AUTO, CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR, CULE_ENGINE_JIT, CULE_ENGINE_VJIT = 0, 1, 2, 3, 4
+ENGINE_NAMES = {CULE_ENGINE_SIMT: "simt", CULE_ENGINE_SCALAR: "scalar", CULE_ENGINE_JIT: "jit",
+                CULE_ENGINE_VJIT: "vjit"}
 
 
 class CuleError(RuntimeError):
@@ -89,12 +90,14 @@ def load():
     L.cule_destroy.argtypes = [vp]
     L.cule_jit_prepare.argtypes = [ctypes.POINTER(u8p), ctypes.POINTER(ctypes.c_size_t), ctypes.c_int, ctypes.c_int,
                                    ctypes.c_char_p, ctypes.c_size_t]
+    L.cule_jit_prepare_engine.argtypes = [ctypes.POINTER(u8p), ctypes.POINTER(ctypes.c_size_t), ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]
     L.cule_last_error.argtypes = []
     L.cule_last_error.restype = ctypes.c_char_p
     for name in ("cule_create", "cule_reset", "cule_step", "cule_step_host", "cule_get_state",
                  "cule_reset_stacked", "cule_step_stacked", "cule_vtrace",
                  "cule_set_state", "cule_counters", "cule_debug_exec", "cule_num_envs",
-                 "cule_frameskip", "cule_engine", "cule_destroy", "cule_jit_prepare"):
+                 "cule_frameskip", "cule_engine", "cule_destroy", "cule_jit_prepare", "cule_jit_prepare_engine"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -112,14 +115,15 @@ def default_config() -> CuleConfig:
     return c
 
 
-def jit_prepare(roms, obs_mode: int = CULE_OBS_GRAY84) -> str:
-    """Translate + compile the JIT step kernel of a ROM set into the on-disk cache (host only,
-    no GPU needed; include/cule.h cule_jit_prepare).  Returns the library's summary line."""
+def jit_prepare(roms, obs_mode: int = CULE_OBS_GRAY84, engine: int = CULE_ENGINE_JIT) -> str:
+    """Translate + compile the step kernel of a translated engine (JIT or VJIT) for a ROM set
+    into the on-disk cache (host only, no GPU needed; include/cule.h cule_jit_prepare_engine).
+    Returns the library's summary line."""
     import numpy as np
     arrs = [np.frombuffer(bytes(r), np.uint8).copy() for r in roms]
     u8p = ctypes.POINTER(ctypes.c_uint8)
     ptrs = (u8p * len(arrs))(*[a.ctypes.data_as(u8p) for a in arrs])
     lens = (ctypes.c_size_t * len(arrs))(*[len(a) for a in arrs])
     buf = ctypes.create_string_buffer(512)
-    check(load().cule_jit_prepare(ptrs, lens, len(arrs), obs_mode, buf, len(buf)))
+    check(load().cule_jit_prepare_engine(ptrs, lens, len(arrs), obs_mode, engine, buf, len(buf)))
     return buf.value.decode()

@@ -21,6 +21,7 @@
 #include "scalar_kernels.cuh"
 #include "vtrace.cuh"
 #include "jit.h"
+#include "vjit_kernels.cuh"
 
 namespace {
 
@@ -121,10 +122,10 @@ RomSet make_romset(const uint8_t* const* roms, const size_t* rom_lens, int n_rom
 }
 
 // translate + compile (or fetch from the caches) the JIT step kernel for a ROM set
-std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, size_t* n_insn, double* secs, bool* from_disk,
-                            std::string& err) {
+std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, size_t* n_insn, double* secs,
+                            bool* from_disk, std::string& err) {
   cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
-  cule::jit::Translation t = tr.run(gray);
+  cule::jit::Translation t = tr.run(gray, simt);
   if (!t.ok) { err = t.why; return {}; }
   *n_insn = t.n_insn;
   if (const char* dump = getenv("CULE_JIT_DUMP")) {
@@ -159,6 +160,9 @@ struct cule_env {
   size_t jit_smem = 0;     // dynamic shared memory of the translated kernel (no records staged)
   size_t jit_insn = 0;
   double jit_compile_s = 0.0;
+  // engine 2: the SIMT translated kernel (vjit_kernels.cuh), vepw envs per warp
+  uint32_t vepw = 32, vblock = 0, vgrid = 0;
+  size_t vsmem = 0;
 };
 
 static cule::Params base_params(const cule_env* e) {
@@ -255,6 +259,7 @@ static int requested_engine(const cule_config* c) {
     if (!strcmp(v, "simt")) return CULE_ENGINE_SIMT;
     if (!strcmp(v, "scalar")) return CULE_ENGINE_SCALAR;
     if (!strcmp(v, "jit")) return CULE_ENGINE_JIT;
+    if (!strcmp(v, "vjit")) return CULE_ENGINE_VJIT;
   }
   return c->engine;
 }
@@ -341,7 +346,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   if (cfg->obs_mode == CULE_OBS_GRAY84 && !cfg->palette_rgb)
     return fail(CULE_E_INVAL, "GRAY84 needs cfg->palette_rgb (384 bytes)");
   if (((uintptr_t)d_workspace & 255) != 0) return fail(CULE_E_INVAL, "workspace must be 256-byte aligned");
-  if (cfg->engine < CULE_ENGINE_AUTO || cfg->engine > CULE_ENGINE_JIT) return fail(CULE_E_INVAL, "bad engine");
+  if (cfg->engine < CULE_ENGINE_AUTO || cfg->engine > CULE_ENGINE_VJIT) return fail(CULE_E_INVAL, "bad engine");
   for (int r = 0; r < n_roms; ++r) {
     if (!roms[r]) return fail(CULE_E_INVAL, "null ROM");
     const size_t n = rom_lens[r];
@@ -377,7 +382,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   e->rom_bytes = off;
   e->epw = choose_epw(num_envs);
   const int want = requested_engine(cfg);
-  e->engine = want == CULE_ENGINE_SIMT ? 0 : (want == CULE_ENGINE_AUTO ? choose_engine(num_envs) : 1);
+  e->engine = (want == CULE_ENGINE_SIMT || want == CULE_ENGINE_VJIT) ? 0
+                                                                    : (want == CULE_ENGINE_AUTO ? choose_engine(num_envs) : 1);
   {
     // records cost 8 B per ROM byte of shared memory: they fit for every combination up to
     // 4 x 4 KB or 2 x F8 + 1 x 4 KB (CULE_NO_REC=1 pretends they do not)
@@ -483,7 +489,53 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   // beyond that the batched engine amortises its datapath over 32 envs per warp and the
   // translated code of several ROMs crowds the instruction cache) and applies (idle skip off)
   const bool jit_auto = want == CULE_ENGINE_AUTO && !cfg->idle_skip && (n_roms == 1 || num_envs <= 16384);
-  if (want == CULE_ENGINE_JIT || jit_auto) {
+  if (want == CULE_ENGINE_VJIT) {
+    std::string jerr;
+    auto& drv = cule::jit::driver();
+    std::vector<char> cubin;
+    bool from_disk = false;
+    if (!drv.ok) jerr = "CUDA driver entry points unavailable";
+    else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
+    else {
+      RomSet rs = make_romset(roms, rom_lens, n_roms);
+      cubin = jit_cubin(rs, n_roms, g, true, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+    }
+    // envs per warp (CULE_VEPW, power of two <= 32) and warps per block: as many warps as the
+    // shared memory holds (one block per SM), no more than the envs need to cover every SM
+    uint32_t vepw = 32;
+    if (const char* v = getenv("CULE_VEPW")) {
+      const int b = atoi(v);
+      if (b >= 1 && b <= 32 && (b & (b - 1)) == 0) vepw = (uint32_t)b;
+    }
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (optin <= 0) optin = 232448;
+    const uint32_t warps = ((uint32_t)num_envs + vepw - 1) / vepw;
+    const uint32_t fit = (uint32_t)(((size_t)optin - cule::vjit_lane_off(e->rom_bytes)) / (32u * 4u * cule::kVLaneWords));
+    uint32_t wpb = (warps + (uint32_t)sm_count() - 1) / (uint32_t)sm_count();
+    if (const char* v = getenv("CULE_VWPB")) wpb = (uint32_t)atoi(v);
+    wpb = std::max(1u, std::min({wpb, fit, (uint32_t)CULE_VWARPS}));
+    e->vepw = vepw;
+    e->vblock = 32u * wpb;
+    e->vgrid = (warps + wpb - 1) / wpb;
+    e->vsmem = cule::vjit_smem_bytes(e->rom_bytes, e->vblock);
+    CUresult cr = CUDA_SUCCESS;
+    if (!cubin.empty()) {
+      cr = drv.moduleLoadData(&e->jit_mod, cubin.data());
+      if (cr == CUDA_SUCCESS) cr = drv.moduleGetFunction(&e->jit_fn, e->jit_mod, "cule_vjit_step");
+      if (cr == CUDA_SUCCESS)
+        cr = drv.funcSetAttribute(e->jit_fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)e->vsmem);
+      if (cr != CUDA_SUCCESS) jerr = "loading the SIMT translated kernel failed (CUresult " + std::to_string((int)cr) + ")";
+    }
+    if (!jerr.empty() || !e->jit_fn) {
+      if (e->jit_mod) drv.moduleUnload(e->jit_mod);
+      delete e;
+      return fail(CULE_E_CUDA, "VJIT engine: " + jerr);
+    }
+    e->jit = true;
+    e->engine = 2;
+  } else if (want == CULE_ENGINE_JIT || jit_auto) {
     std::string jerr;
     bool from_disk = false;
     std::vector<char> cubin;
@@ -492,7 +544,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
     else {
       RomSet rs = make_romset(roms, rom_lens, n_roms);
-      cubin = jit_cubin(rs, n_roms, g, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+      cubin = jit_cubin(rs, n_roms, g, false, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
     }
     CUresult cr = CUDA_SUCCESS;
     if (!cubin.empty()) {
@@ -560,6 +612,15 @@ static int launch_step(cule_env* e, const uint8_t* d_actions, void* d_obs, int32
   }
   p.rewards = d_rewards;
   p.dones = d_dones;
+  if (e->engine == 2) {
+    p.use_rec = 0u;
+    p.epw = e->vepw;
+    void* args[] = {&p};
+    const CUresult cr = cule::jit::driver().launchKernel(e->jit_fn, e->vgrid, 1, 1, e->vblock, 1, 1, (unsigned)e->vsmem,
+                                                         (CUstream)s, args, nullptr);
+    if (cr != CUDA_SUCCESS) return fail(CULE_E_CUDA, "cule_vjit_step launch failed (CUresult " + std::to_string((int)cr) + ")");
+    return cuda_check("cule_vjit_step");
+  }
   if (e->engine == 1) {
     const uint32_t sg = e->sgrid;
     // the persistent kernel's work tickets start from zero on the launch stream (the kernel also
@@ -709,20 +770,28 @@ int cule_num_envs(const cule_env* e) { return live(e) ? e->N : CULE_E_CLOSED; }
 int cule_frameskip(const cule_env* e) { return live(e) ? e->fs : CULE_E_CLOSED; }
 int cule_engine(const cule_env* e) {
   if (!live(e)) return CULE_E_CLOSED;
+  if (e->engine == 2) return CULE_ENGINE_VJIT;
   return e->engine == 0 ? CULE_ENGINE_SIMT : (e->jit ? CULE_ENGINE_JIT : CULE_ENGINE_SCALAR);
 }
 
 int cule_jit_prepare(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int obs_mode, char* info,
                      size_t info_len) {
+  return cule_jit_prepare_engine(roms, rom_lens, n_roms, obs_mode, CULE_ENGINE_JIT, info, info_len);
+}
+
+int cule_jit_prepare_engine(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int obs_mode,
+                            int engine, char* info, size_t info_len) {
   int rc = check_roms(roms, rom_lens, n_roms);
   if (rc) return rc;
   if (obs_mode != CULE_OBS_RAW && obs_mode != CULE_OBS_GRAY84) return fail(CULE_E_INVAL, "bad obs_mode");
+  if (engine != CULE_ENGINE_JIT && engine != CULE_ENGINE_VJIT) return fail(CULE_E_INVAL, "engine must be JIT or VJIT");
   RomSet rs = make_romset(roms, rom_lens, n_roms);
   size_t n_insn = 0;
   double secs = 0.0;
   bool from_disk = false;
   std::string err;
-  std::vector<char> cubin = jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, &n_insn, &secs, &from_disk, err);
+  std::vector<char> cubin =
+      jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, engine == CULE_ENGINE_VJIT, &n_insn, &secs, &from_disk, err);
   if (cubin.empty()) return fail(CULE_E_CUDA, "JIT: " + err);
   if (info && info_len) {
     snprintf(info, info_len, "%zu instructions translated, cubin %zu bytes, %s %.1f s, cache %s", n_insn,

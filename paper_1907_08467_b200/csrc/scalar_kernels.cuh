@@ -168,7 +168,7 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
   for (;;) {
     uint32_t ev = SE_NONE;
     if (lane == 0u) {
-#ifdef CULE_JIT
+#if defined(CULE_JIT) && !defined(CULE_VJIT)
       // the translated engine (jit.h): the ROMs' code compiled into run_cpu_jit (no debug entry)
       ev = run_cpu_jit(M, rom_s, dtab_s, ram_s, lg_s, kSLogCap - 3u, cap_cycles);
       (void)budget;

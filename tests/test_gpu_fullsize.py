@@ -125,7 +125,7 @@ def check_full_size(roms, N, engine, base_set, n_resets, window_ids, T=310, wind
     return len(track), n_done_tracked
 
 
-@pytest.mark.parametrize("engine", ["jit", "scalar"])
+@pytest.mark.parametrize("engine", ["jit", "scalar", "vjit"])
 def test_cfg2_full_trajectory_and_windows(engine):
     N = 4096
     base = np.union1d(np.arange(256), np.arange(0, N, 256))
@@ -133,7 +133,7 @@ def test_cfg2_full_trajectory_and_windows(engine):
     assert n_track >= len(base) + 200 and n_done >= 256   # the resets overlap the base set a little
 
 
-@pytest.mark.parametrize("engine", ["simt", "jit"])
+@pytest.mark.parametrize("engine", ["simt", "jit", "vjit"])
 def test_cfg4_full_trajectory_and_windows(engine):
     N = 32768
     roms = [games.build_rom(n) for n in ("R1", "R2", "R3", "R4")]

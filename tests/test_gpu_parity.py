@@ -14,18 +14,21 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.fixture(autouse=True, params=["simt", "scalar", "jit"])
+@pytest.fixture(autouse=True, params=["simt", "scalar", "jit", "vjit"])
 def engine(request, monkeypatch):
-    """Every parity test runs on all three engines: the batched SIMT datapath, the scalar engine
-    (one env per warp, record-driven interpreter, warp-cooperative TIA replay) and the JIT
-    engine (the scalar engine with the cartridge code translated to CUDA, csrc/jit.h)."""
+    """Every parity test runs on all four engines: the batched SIMT datapath, the scalar engine
+    (one env per warp, record-driven interpreter, warp-cooperative TIA replay), the JIT
+    engine (the scalar engine with the cartridge code translated to CUDA, csrc/jit.h) and the
+    VJIT engine (one env per lane running the translated code, block-scheduled by warp vote,
+    csrc/vjit_kernels.cuh)."""
     monkeypatch.setenv("CULE_ENGINE", request.param)
     return request.param
 
 
 def skip_jit_debug(engine):
-    if engine == "jit":
-        pytest.skip("debug-entry test: the JIT engine's debug_exec runs the scalar interpreter (tested as 'scalar')")
+    if engine in ("jit", "vjit"):
+        pytest.skip("debug-entry test: the translated engines' debug_exec runs an interpreter (tested as "
+                    "'scalar' / 'simt')")
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -109,10 +112,13 @@ def test_mixed_roms_ragged():
 
 @pytest.mark.parametrize("epw", ["1", "4", "32"])
 def test_launch_shape_independence(epw, monkeypatch):
-    """Results do not depend on the launch shape: envs per warp (CULE_EPW), block size and
-    the ROM-grouped env-to-lane permutation (S:283-286 worker-count independence)."""
+    """Results do not depend on the launch shape: envs per warp (CULE_EPW; CULE_VEPW for the
+    VJIT engine), block size and the ROM-grouped env-to-lane permutation (S:283-286
+    worker-count independence)."""
     monkeypatch.setenv("CULE_EPW", epw)
+    monkeypatch.setenv("CULE_VEPW", epw)
     monkeypatch.setenv("CULE_BLOCK", "64")
+    monkeypatch.setenv("CULE_VWPB", "2")
     roms = [games.build_rom(n) for n in ("R1", "R3", "R2")]
     gpu, ref = pair(roms, 77, 4, reset_cache_size=4, env_index_base=5)
     run_parity(gpu, ref, 12, check_every=4)
@@ -440,8 +446,8 @@ def test_idle_skip_is_exact(src, engine):
     """The exact idle-loop skip (cule_config.idle_skip; R#24) skips
     whole [timer read; branch back] poll iterations in closed form: observations, rewards,
     dones, counters and the full state stay bit-identical to the oracle, which never skips."""
-    if engine == "jit":
-        pytest.skip("the JIT engine has no idle-loop skip (cule_create rejects the combination)")
+    if engine in ("jit", "vjit"):
+        pytest.skip("the translated engines have no idle-loop skip (cule_create rejects the combination)")
     import oracle
     from paper_1907_08467_b200 import Env
     rom = games.build_rom(src) if src.startswith("R") else micro.build(
