@@ -613,8 +613,10 @@ def run_cule(args, rank, world, local_rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": desc, "envs_per_gpu": envs, "frameskip": fs, "obs": mode,
                    "actions": "uniform random over 18, torch cuda generator seed 1234+rank",
-                   "l2": ("per-step working set vs 126 MB L2: staged gray frame fs-1 " +
-                          f"{envs * 33600 / 1e6:.0f} MB (scalar engine; 2 frames for simt) + obs " +
+                   "l2": ("per-step working set vs 126 MB L2: staged gray frames " +
+                          f"{envs * 33600 * (1 if env.engine in ('jit', 'scalar') else 2) / 1e6:.0f} MB "
+                          "(frame fs-1 for the one-env-per-warp engines jit/scalar; fs-1 and fs for "
+                          "vjit/simt) + obs " +
                           f"{envs * (7056 if mode == 'gray84' else 33600) / 1e6:.0f} MB + state " +
                           f"{envs * 256 / 1e6:.0f} MB; no flush between steps"),
                    "parallelism": f"dp{world} (env shards)", "engine": env.engine},

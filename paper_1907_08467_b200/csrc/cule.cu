@@ -488,8 +488,15 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   // profiles/r02_engine_sweep.txt: one ROM at every env count; mixed ROM sets up to 16384 envs —
   // beyond that the batched engine amortises its datapath over 32 envs per warp and the
   // translated code of several ROMs crowds the instruction cache) and applies (idle skip off)
-  const bool jit_auto = want == CULE_ENGINE_AUTO && !cfg->idle_skip && (n_roms == 1 || num_envs <= 16384);
-  if (want == CULE_ENGINE_VJIT) {
+  // translated engines (measured sweep, profiles/r02_vjit_sweep.txt): VJIT (one env per lane)
+  // once there are enough envs to fill warps of 16-32 lanes on every SM — 16384+ envs, or 8192+
+  // when several ROMs make the one-env-per-warp engine's replay the larger cost — else JIT
+  // (one env per warp) for one ROM at any count and mixed sets up to 16384 envs; neither has the
+  // idle-loop skip
+  const bool xlate = !cfg->idle_skip;
+  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && (num_envs >= 16384 || (n_roms > 1 && num_envs >= 8192));
+  bool jit_auto = want == CULE_ENGINE_AUTO && xlate && !vjit_auto && (n_roms == 1 || num_envs <= 16384);
+  if (want == CULE_ENGINE_VJIT || vjit_auto) {
     std::string jerr;
     auto& drv = cule::jit::driver();
     std::vector<char> cubin;
@@ -500,9 +507,10 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
       RomSet rs = make_romset(roms, rom_lens, n_roms);
       cubin = jit_cubin(rs, n_roms, g, true, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
     }
-    // envs per warp (CULE_VEPW, power of two <= 32) and warps per block: as many warps as the
-    // shared memory holds (one block per SM), no more than the envs need to cover every SM
-    uint32_t vepw = 32;
+    // envs per warp (CULE_VEPW overrides: power of two <= 32; measured: 32 from 32768 envs, 16
+    // from 8192, else 8) and warps per block: as many warps as the envs need to cover every SM,
+    // within the shared memory of one block per SM
+    uint32_t vepw = num_envs >= 32768 ? 32u : (num_envs >= 8192 ? 16u : 8u);
     if (const char* v = getenv("CULE_VEPW")) {
       const int b = atoi(v);
       if (b >= 1 && b <= 32 && (b & (b - 1)) == 0) vepw = (uint32_t)b;
@@ -528,13 +536,22 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
         cr = drv.funcSetAttribute(e->jit_fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)e->vsmem);
       if (cr != CUDA_SUCCESS) jerr = "loading the SIMT translated kernel failed (CUresult " + std::to_string((int)cr) + ")";
     }
-    if (!jerr.empty() || !e->jit_fn) {
+    if (jerr.empty() && e->jit_fn) {
+      e->jit = true;
+      e->engine = 2;
+    } else if (want == CULE_ENGINE_VJIT) {
       if (e->jit_mod) drv.moduleUnload(e->jit_mod);
       delete e;
       return fail(CULE_E_CUDA, "VJIT engine: " + jerr);
+    } else {  // AUTO: the interpreter engines (the translation did not apply)
+      if (e->jit_mod) drv.moduleUnload(e->jit_mod);
+      e->jit_mod = nullptr;
+      e->jit_fn = nullptr;
+      jit_auto = false;
     }
-    e->jit = true;
-    e->engine = 2;
+  }
+  if (e->engine == 2) {
+    // the SIMT translated engine runs
   } else if (want == CULE_ENGINE_JIT || jit_auto) {
     std::string jerr;
     bool from_disk = false;

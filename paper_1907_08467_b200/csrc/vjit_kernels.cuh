@@ -33,6 +33,61 @@ __host__ __device__ __forceinline__ size_t vjit_smem_bytes(uint32_t rom_bytes, u
 }
 
 #ifdef CULE_VJIT  // the device code lives in the generated module (it calls run_cpu_vjit)
+// GRAY84 observation of one env from its staged gray frames fs (fa) and fs-1 (fb; null for
+// fs = 1), by the whole warp: rows in groups of five (group g closes output rows 2g and 2g+1),
+// 16-byte loads of both frames (the next group's loads in flight while this one is reduced),
+// byte max into an 800-byte shared buffer, then the exact area weights — packed per column
+// (area84_col) and 2:2:1 / 1:2:2 over rows, total 200, round half to even (R#16, R#17; the
+// same arithmetic as kernels.cuh warp_area84, which reads single bytes from HBM).
+__device__ __forceinline__ void warp_area84_staged(const uint8_t* fa, const uint8_t* fb, uint8_t* out, uint32_t lane,
+                                                   uint32_t buf_s, uint32_t cols_s) {
+  const uint4* A = reinterpret_cast<const uint4*>(fa);
+  const uint4* B = reinterpret_cast<const uint4*>(fb);
+  constexpr uint32_t kG = 50u;  // 16-byte chunks per five rows
+  uint4 a0, b0, a1 = make_uint4(0, 0, 0, 0), b1 = a1;
+  auto load = [&](uint32_t g) {
+    const uint32_t q = g * kG + lane;
+    a0 = A[q];
+    b0 = fb ? B[q] : a0;
+    if (lane < kG - 32u) {
+      a1 = A[q + 32u];
+      b1 = fb ? B[q + 32u] : a1;
+    }
+  };
+  auto vmax = [](uint4 x, uint4 y) {
+    return make_uint4(__vmaxu4(x.x, y.x), __vmaxu4(x.y, y.y), __vmaxu4(x.z, y.z), __vmaxu4(x.w, y.w));
+  };
+  load(0);
+  for (uint32_t g = 0; g < 42u; ++g) {
+    const uint4 m0 = vmax(a0, b0), m1 = vmax(a1, b1);
+    __syncwarp();  // the previous group's reads of the buffer are done
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(buf_s + 16u * lane), "r"(m0.x), "r"(m0.y),
+                 "r"(m0.z), "r"(m0.w) : "memory");
+    if (lane < kG - 32u)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(buf_s + 16u * (lane + 32u)), "r"(m1.x),
+                   "r"(m1.y), "r"(m1.z), "r"(m1.w) : "memory");
+    if (g + 1u < 42u) load(g + 1u);
+    __syncwarp();
+    for (uint32_t o = lane; o < 168u; o += 32u) {
+      const uint32_t odd = o >= 84u ? 1u : 0u, j = o - 84u * odd;
+      uint32_t cw;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(cols_s + 4u * j) : "memory");
+      const uint32_t c0 = cw & 0xFFu, wc0 = (cw >> 8) & 0xFFu, wc1 = (cw >> 16) & 0xFFu, wc2 = cw >> 24;
+      const uint32_t c2 = wc2 ? c0 + 2u : c0;
+      const uint32_t q0 = buf_s + (odd ? 320u : 0u) + c0;
+      const uint32_t s0 = wc0 * lds_u8(q0) + wc1 * lds_u8(q0 + 1u) + wc2 * lds_u8(q0 + (c2 - c0));
+      const uint32_t s1 = wc0 * lds_u8(q0 + 160u) + wc1 * lds_u8(q0 + 161u) + wc2 * lds_u8(q0 + 160u + (c2 - c0));
+      const uint32_t s2 = wc0 * lds_u8(q0 + 320u) + wc1 * lds_u8(q0 + 321u) + wc2 * lds_u8(q0 + 320u + (c2 - c0));
+      const uint32_t S = (odd ? 1u : 2u) * s0 + 2u * s1 + (odd ? 2u : 1u) * s2;
+      uint32_t q = S / 200u;
+      const uint32_t r = S - 200u * q;
+      q += (r > 100u || (r == 100u && (q & 1u))) ? 1u : 0u;
+      out[(2u * g + odd) * 84u + j] = (uint8_t)q;
+    }
+  }
+  __syncwarp();
+}
+
 // frames of one step for the lanes of a warp (all 32 lanes call it together)
 template <bool kGray>
 __device__ __forceinline__ int32_t simulate_v(SMach* M, uint32_t* tw, uint32_t* pw, const uint32_t* lg, bool active,
@@ -172,7 +227,11 @@ __device__ __forceinline__ void vjit_kernel_body(const Params& p) {
     if (n_done) atomicAdd(&p.counters[2], (unsigned long long)(long long)ret_sum);
     if (n_fault) atomicAdd(&p.counters[3], (unsigned long long)n_fault);
   }
-  // a5: warp-cooperative observation epilogue, one env at a time
+  // a5: warp-cooperative observation epilogue, one env at a time; the warp's lane areas are
+  // free now (state stored) and serve as the 800-byte reduction buffer
+  __syncwarp();
+  const uint32_t buf_s = smem_addr(lw - threadIdx.x * kVLaneWords + (threadIdx.x & ~31u) * kVLaneWords);
+  const uint32_t cols_s = smem_addr(smem + kSmCols);
   for (uint32_t l = 0; l < 32u; ++l) {
     if (!((amask >> l) & 1u)) continue;
     const uint32_t env = __shfl_sync(kFull, i, l);
@@ -185,7 +244,7 @@ __device__ __forceinline__ void vjit_kernel_body(const Params& p) {
       if (f) warp_zero(o, kObs84, lane);
       else {
         const uint8_t* pair = p.staging + (size_t)env * (2 * kFrameBytes);
-        warp_area84(pair + kFrameBytes, p.fs >= 2 ? pair : nullptr, o, lane);
+        warp_area84_staged(pair + kFrameBytes, p.fs >= 2 ? pair : nullptr, o, lane, buf_s, cols_s);
       }
     } else if (f) {
       warp_zero(p.obs + (size_t)env * kFrameBytes, kFrameBytes, lane);
