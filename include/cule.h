@@ -77,7 +77,7 @@ typedef struct {
   const uint8_t* palette_rgb; /* HOST, 128 x (R,G,B) NTSC palette; read only during
                                  cule_create; required for GRAY84 (gray LUT), ignored for RAW  */
   int32_t engine;             /* CULE_ENGINE_AUTO (default) or one of the engines below; the
-                                 environment variable CULE_ENGINE (simt|scalar|jit|vjit) overrides */
+                                 environment variable CULE_ENGINE (simt|scalar|jit|vjit|wsvjit) overrides */
 } cule_config;
 
 /* Engines (all compute the same results, bit for bit):
@@ -87,7 +87,9 @@ typedef struct {
  *          compiled with NVRTC for sm_100a (static recompilation; cached on disk by content);
  *   VJIT   one env per lane running the translated code (up to 32 envs per warp), basic
  *          blocks scheduled by warp vote so lanes at the same PC run together; per-lane TIA
- *          replay (the SIMT engine's renderer).
+ *          replay (the SIMT engine's renderer);
+ *   WSVJIT VJIT with warp specialization: warp pairs share 32 envs, the producer warp emulates
+ *          into double-buffered TIA logs, the consumer warp replays and renders (mbarriers).
  * AUTO picks among them by env count (cule.cu choose_engine, measured); an engine that does
  * not apply (idle_skip on, translation too large) falls back to SCALAR / SIMT. */
 #define CULE_ENGINE_AUTO 0
@@ -95,6 +97,7 @@ typedef struct {
 #define CULE_ENGINE_SCALAR 2
 #define CULE_ENGINE_JIT 3
 #define CULE_ENGINE_VJIT 4
+#define CULE_ENGINE_WSVJIT 5
 
 /* Fill *cfg with the defaults above (score $80/$81, terminal $82 bit 0, seed 0, base 0). */
 void cule_default_config(cule_config* cfg);
@@ -179,8 +182,8 @@ int cule_debug_exec(cule_env* env, int n_instr, int32_t* d_status, void* cuda_st
 
 /* Number of envs / frameskip / observation bytes per env of a handle. */
 int cule_num_envs(const cule_env* env);
-/* Which step kernel the handle runs: CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR, CULE_ENGINE_JIT or
- * CULE_ENGINE_VJIT (see cule_config.engine).  CULE_E_CLOSED for a destroyed handle. */
+/* Which step kernel the handle runs: CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR, CULE_ENGINE_JIT,
+ * CULE_ENGINE_VJIT or CULE_ENGINE_WSVJIT (see cule_config.engine).  CULE_E_CLOSED for a destroyed handle. */
 int cule_engine(const cule_env* env);
 
 /* Host only (no GPU needed): translate the ROM set (as cule_create would for the JIT engine)
@@ -191,8 +194,9 @@ int cule_engine(const cule_env* env);
  * cule_last_error). */
 int cule_jit_prepare(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int obs_mode, char* info,
                      size_t info_len);
-/* Same for a given translated engine: CULE_ENGINE_JIT (as cule_jit_prepare) or CULE_ENGINE_VJIT
- * (the SIMT translation).  CULE_E_INVAL for any other engine. */
+/* Same for a given translated engine: CULE_ENGINE_JIT (as cule_jit_prepare), CULE_ENGINE_VJIT
+ * (the SIMT translation) or CULE_ENGINE_WSVJIT (its warp-specialized kernel).  CULE_E_INVAL for
+ * any other engine. */
 int cule_jit_prepare_engine(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, int obs_mode,
                             int engine, char* info, size_t info_len);
 int cule_frameskip(const cule_env* env);

@@ -42,8 +42,9 @@ class CuleConfig(ctypes.Structure):
                 ("engine", ctypes.c_int32)]
 
 CULE_ENGINE_AUTO, CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR, CULE_ENGINE_JIT, CULE_ENGINE_VJIT = 0, 1, 2, 3, 4
+CULE_ENGINE_WSVJIT = 5
 ENGINE_NAMES = {CULE_ENGINE_SIMT: "simt", CULE_ENGINE_SCALAR: "scalar", CULE_ENGINE_JIT: "jit",
-                CULE_ENGINE_VJIT: "vjit"}
+                CULE_ENGINE_VJIT: "vjit", CULE_ENGINE_WSVJIT: "wsvjit"}
 
 
 class CuleError(RuntimeError):

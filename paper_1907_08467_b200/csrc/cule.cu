@@ -122,10 +122,10 @@ RomSet make_romset(const uint8_t* const* roms, const size_t* rom_lens, int n_rom
 }
 
 // translate + compile (or fetch from the caches) the JIT step kernel for a ROM set
-std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, size_t* n_insn, double* secs,
-                            bool* from_disk, std::string& err) {
+std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, bool ws, size_t* n_insn,
+                            double* secs, bool* from_disk, std::string& err) {
   cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
-  cule::jit::Translation t = tr.run(gray, simt);
+  cule::jit::Translation t = tr.run(gray, simt, ws);
   if (!t.ok) { err = t.why; return {}; }
   *n_insn = t.n_insn;
   if (const char* dump = getenv("CULE_JIT_DUMP")) {
@@ -162,6 +162,7 @@ struct cule_env {
   double jit_compile_s = 0.0;
   // engine 2: the SIMT translated kernel (vjit_kernels.cuh), vepw envs per warp
   uint32_t vepw = 32, vblock = 0, vgrid = 0;
+  bool vws = false;        // the warp-specialized variant (producer / consumer warp pairs)
   size_t vsmem = 0;
 };
 
@@ -260,6 +261,7 @@ static int requested_engine(const cule_config* c) {
     if (!strcmp(v, "scalar")) return CULE_ENGINE_SCALAR;
     if (!strcmp(v, "jit")) return CULE_ENGINE_JIT;
     if (!strcmp(v, "vjit")) return CULE_ENGINE_VJIT;
+    if (!strcmp(v, "wsvjit")) return CULE_ENGINE_WSVJIT;
   }
   return c->engine;
 }
@@ -346,7 +348,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   if (cfg->obs_mode == CULE_OBS_GRAY84 && !cfg->palette_rgb)
     return fail(CULE_E_INVAL, "GRAY84 needs cfg->palette_rgb (384 bytes)");
   if (((uintptr_t)d_workspace & 255) != 0) return fail(CULE_E_INVAL, "workspace must be 256-byte aligned");
-  if (cfg->engine < CULE_ENGINE_AUTO || cfg->engine > CULE_ENGINE_VJIT) return fail(CULE_E_INVAL, "bad engine");
+  if (cfg->engine < CULE_ENGINE_AUTO || cfg->engine > CULE_ENGINE_WSVJIT) return fail(CULE_E_INVAL, "bad engine");
   for (int r = 0; r < n_roms; ++r) {
     if (!roms[r]) return fail(CULE_E_INVAL, "null ROM");
     const size_t n = rom_lens[r];
@@ -382,7 +384,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   e->rom_bytes = off;
   e->epw = choose_epw(num_envs);
   const int want = requested_engine(cfg);
-  e->engine = (want == CULE_ENGINE_SIMT || want == CULE_ENGINE_VJIT) ? 0
+  e->engine = (want == CULE_ENGINE_SIMT || want == CULE_ENGINE_VJIT || want == CULE_ENGINE_WSVJIT) ? 0
                                                                     : (want == CULE_ENGINE_AUTO ? choose_engine(num_envs) : 1);
   {
     // records cost 8 B per ROM byte of shared memory: they fit for every combination up to
@@ -496,7 +498,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   const bool xlate = !cfg->idle_skip;
   const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && (num_envs >= 16384 || (n_roms > 1 && num_envs >= 8192));
   bool jit_auto = want == CULE_ENGINE_AUTO && xlate && !vjit_auto && (n_roms == 1 || num_envs <= 16384);
-  if (want == CULE_ENGINE_VJIT || vjit_auto) {
+  if (want == CULE_ENGINE_VJIT || want == CULE_ENGINE_WSVJIT || vjit_auto) {
+    const bool ws = want == CULE_ENGINE_WSVJIT;
     std::string jerr;
     auto& drv = cule::jit::driver();
     std::vector<char> cubin;
@@ -505,7 +508,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
     else {
       RomSet rs = make_romset(roms, rom_lens, n_roms);
-      cubin = jit_cubin(rs, n_roms, g, true, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+      cubin = jit_cubin(rs, n_roms, g, true, ws, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
     }
     // envs per warp (CULE_VEPW overrides: power of two <= 32; measured: 32 from 32768 envs, 16
     // from 8192, else 8) and warps per block: as many warps as the envs need to cover every SM,
@@ -519,19 +522,23 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (optin <= 0) optin = 232448;
+    // (warp-specialized: groups of envs per warp PAIR, which shares one set of lane areas)
     const uint32_t warps = ((uint32_t)num_envs + vepw - 1) / vepw;
-    const uint32_t fit = (uint32_t)(((size_t)optin - cule::vjit_lane_off(e->rom_bytes)) / (32u * 4u * cule::kVLaneWords));
+    const size_t lane_off = ws ? cule::wsvjit_lane_off(e->rom_bytes) : cule::vjit_lane_off(e->rom_bytes);
+    const uint32_t fit = (uint32_t)(((size_t)optin - lane_off) /
+                                    (32u * 4u * (ws ? cule::kWLaneWords : cule::kVLaneWords)));
     uint32_t wpb = (warps + (uint32_t)sm_count() - 1) / (uint32_t)sm_count();
     if (const char* v = getenv("CULE_VWPB")) wpb = (uint32_t)atoi(v);
-    wpb = std::max(1u, std::min({wpb, fit, (uint32_t)CULE_VWARPS}));
+    wpb = std::max(1u, std::min({wpb, fit, (uint32_t)CULE_VWARPS / (ws ? 2u : 1u)}));
     e->vepw = vepw;
-    e->vblock = 32u * wpb;
+    e->vws = ws;
+    e->vblock = (ws ? 64u : 32u) * wpb;
     e->vgrid = (warps + wpb - 1) / wpb;
-    e->vsmem = cule::vjit_smem_bytes(e->rom_bytes, e->vblock);
+    e->vsmem = ws ? cule::wsvjit_smem_bytes(e->rom_bytes, wpb) : cule::vjit_smem_bytes(e->rom_bytes, e->vblock);
     CUresult cr = CUDA_SUCCESS;
     if (!cubin.empty()) {
       cr = drv.moduleLoadData(&e->jit_mod, cubin.data());
-      if (cr == CUDA_SUCCESS) cr = drv.moduleGetFunction(&e->jit_fn, e->jit_mod, "cule_vjit_step");
+      if (cr == CUDA_SUCCESS) cr = drv.moduleGetFunction(&e->jit_fn, e->jit_mod, ws ? "cule_vjit_ws_step" : "cule_vjit_step");
       if (cr == CUDA_SUCCESS)
         cr = drv.funcSetAttribute(e->jit_fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)e->vsmem);
       if (cr != CUDA_SUCCESS) jerr = "loading the SIMT translated kernel failed (CUresult " + std::to_string((int)cr) + ")";
@@ -539,10 +546,10 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     if (jerr.empty() && e->jit_fn) {
       e->jit = true;
       e->engine = 2;
-    } else if (want == CULE_ENGINE_VJIT) {
+    } else if (want == CULE_ENGINE_VJIT || want == CULE_ENGINE_WSVJIT) {
       if (e->jit_mod) drv.moduleUnload(e->jit_mod);
       delete e;
-      return fail(CULE_E_CUDA, "VJIT engine: " + jerr);
+      return fail(CULE_E_CUDA, std::string(ws ? "WSVJIT" : "VJIT") + " engine: " + jerr);
     } else {  // AUTO: the interpreter engines (the translation did not apply)
       if (e->jit_mod) drv.moduleUnload(e->jit_mod);
       e->jit_mod = nullptr;
@@ -561,7 +568,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
     else {
       RomSet rs = make_romset(roms, rom_lens, n_roms);
-      cubin = jit_cubin(rs, n_roms, g, false, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+      cubin = jit_cubin(rs, n_roms, g, false, false, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
     }
     CUresult cr = CUDA_SUCCESS;
     if (!cubin.empty()) {
@@ -787,7 +794,7 @@ int cule_num_envs(const cule_env* e) { return live(e) ? e->N : CULE_E_CLOSED; }
 int cule_frameskip(const cule_env* e) { return live(e) ? e->fs : CULE_E_CLOSED; }
 int cule_engine(const cule_env* e) {
   if (!live(e)) return CULE_E_CLOSED;
-  if (e->engine == 2) return CULE_ENGINE_VJIT;
+  if (e->engine == 2) return e->vws ? CULE_ENGINE_WSVJIT : CULE_ENGINE_VJIT;
   return e->engine == 0 ? CULE_ENGINE_SIMT : (e->jit ? CULE_ENGINE_JIT : CULE_ENGINE_SCALAR);
 }
 
@@ -801,14 +808,16 @@ int cule_jit_prepare_engine(const uint8_t* const* roms, const size_t* rom_lens, 
   int rc = check_roms(roms, rom_lens, n_roms);
   if (rc) return rc;
   if (obs_mode != CULE_OBS_RAW && obs_mode != CULE_OBS_GRAY84) return fail(CULE_E_INVAL, "bad obs_mode");
-  if (engine != CULE_ENGINE_JIT && engine != CULE_ENGINE_VJIT) return fail(CULE_E_INVAL, "engine must be JIT or VJIT");
+  if (engine != CULE_ENGINE_JIT && engine != CULE_ENGINE_VJIT && engine != CULE_ENGINE_WSVJIT)
+    return fail(CULE_E_INVAL, "engine must be JIT, VJIT or WSVJIT");
   RomSet rs = make_romset(roms, rom_lens, n_roms);
   size_t n_insn = 0;
   double secs = 0.0;
   bool from_disk = false;
   std::string err;
   std::vector<char> cubin =
-      jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, engine == CULE_ENGINE_VJIT, &n_insn, &secs, &from_disk, err);
+      jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, engine != CULE_ENGINE_JIT, engine == CULE_ENGINE_WSVJIT, &n_insn,
+                &secs, &from_disk, err);
   if (cubin.empty()) return fail(CULE_E_CUDA, "JIT: " + err);
   if (info && info_len) {
     snprintf(info, info_len, "%zu instructions translated, cubin %zu bytes, %s %.1f s, cache %s", n_insn,

@@ -338,7 +338,9 @@ __device__ __forceinline__ uint32_t collide_coop(const Words& w, uint32_t lane, 
   return __reduce_or_sync(0xFFFFFFFFu, bits);
 }
 
-// the 16 pixels of the lane's chunk (4 words of 4 bytes) with the registers of the current span
+// the 16 pixels of the lane's chunk (4 words of 4 bytes) with the registers of the current span:
+// priority (R#13) resolved on the chunk's 16-bit coverage masks into a 3-bit colour index per
+// pixel, turned into byte-permute selectors (tia.cuh render_span does the same per lane)
 __device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t lane, uint32_t shade_s,
                                          uint32_t& x0w, uint32_t& x1w, uint32_t& x2w, uint32_t& x3w) {
   // the four shaded colour words (COLUP0, COLUP1, COLUPF, COLUBK), kept current by flush_coop
@@ -346,20 +348,23 @@ __device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(c0), "=r"(c1), "=r"(cbl), "=r"(cbk) : "r"(shade_s) : "memory");
   const uint32_t ctrlpf = byte_of(t.w1, 3);
   const uint32_t cp = (ctrlpf & 2u) ? (lane < 5u ? c0 : c1) : cbl;  // score mode: P0/P1 colour per half
+  // permute source bytes: 0 background, 1 playfield, 2 P0/M0, 3 P1/M1, 4 ball (COLUPF)
+  const uint32_t X = __byte_perm(__byte_perm(cbk, cp, 0x0040u), __byte_perm(c0, c1, 0x0040u), 0x5410u);
   const uint32_t hs = 16u * (lane & 1u);
-  const uint32_t q0 = (w.p0 | w.m0) >> hs, q1 = (w.p1 | w.m1) >> hs, qb = w.bl >> hs, qp = w.pf >> hs;
-  if (((q0 | q1 | qb) & 0xFFFFu) == 0u) {
-    x0w = cbk ^ ((cbk ^ cp) & nib_bytes(qp));
-    x1w = cbk ^ ((cbk ^ cp) & nib_bytes(qp >> 4));
-    x2w = cbk ^ ((cbk ^ cp) & nib_bytes(qp >> 8));
-    x3w = cbk ^ ((cbk ^ cp) & nib_bytes(qp >> 12));
+  const uint32_t a = (w.p0 | w.m0) >> hs, b = (w.p1 | w.m1) >> hs, l = w.bl >> hs, f = w.pf >> hs;
+  uint32_t e0, e1, eb, ep;
+  if (!(ctrlpf & 4u)) {
+    e0 = a; e1 = b & ~a; eb = l & ~(a | b); ep = f & ~(a | b | l);
   } else {
-    const bool pfp = (ctrlpf & 4u) != 0u;
-    x0w = Tia::group_px(q0, q1, qb, qp, 0u, pfp, c0, c1, cbl, cp, cbk);
-    x1w = Tia::group_px(q0, q1, qb, qp, 4u, pfp, c0, c1, cbl, cp, cbk);
-    x2w = Tia::group_px(q0, q1, qb, qp, 8u, pfp, c0, c1, cbl, cp, cbk);
-    x3w = Tia::group_px(q0, q1, qb, qp, 12u, pfp, c0, c1, cbl, cp, cbk);
+    eb = l; ep = f & ~l; e0 = a & ~(l | f); e1 = b & ~(l | f | a);
   }
+  const uint32_t i0 = ep | e1, i1 = e0 | e1, i2 = eb;
+  const uint32_t sa = Tia::sel_bits(i0) | (Tia::sel_bits(i1) << 1) | (Tia::sel_bits(i2) << 2);
+  const uint32_t sb = Tia::sel_bits(i0 >> 8) | (Tia::sel_bits(i1 >> 8) << 1) | (Tia::sel_bits(i2 >> 8) << 2);
+  x0w = __byte_perm(X, cbl, sa);
+  x1w = __byte_perm(X, cbl, sa >> 16);
+  x2w = __byte_perm(X, cbl, sb);
+  x3w = __byte_perm(X, cbl, sb >> 16);
 }
 
 // store the completed row and start the next

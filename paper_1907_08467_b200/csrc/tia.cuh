@@ -81,6 +81,11 @@ struct PixWriter {
     w2 = (w2 & ~m2) | (p2 & m2);
     w3 = (w3 & ~m3) | (p3 & m3);
   }
+  // a chunk whose 16 pixels all lie in the span
+  __device__ __forceinline__ void emit_full(int32_t c, uint32_t p0, uint32_t p1, uint32_t p2, uint32_t p3) {
+    if (c != chunk) advance_to(c);
+    w0 = p0; w1 = p1; w2 = p2; w3 = p3;
+  }
   __device__ __forceinline__ void load(const uint32_t* w, uint32_t s) {
     base = reinterpret_cast<uint8_t*>((uint64_t)w[0] | ((uint64_t)w[s] << 32));
     chunk = (int32_t)w[2 * s];
@@ -263,31 +268,66 @@ struct Tia {
     return (c0 & B0) | (c1 & B1) | (cbl & Bb) | (cp & Bp) | (cbk & ~(B0 | B1 | Bb | Bp));
   }
 
-  // pixels [xa, xb) of window row `row`, one 16-pixel chunk (4 groups) per iteration
+  // one palette byte (gray value in GRAY84, palette index in RAW)
+  __device__ __forceinline__ static uint32_t shade1(uint32_t colu, const uint8_t* gray) {
+    const uint32_t idx = (colu >> 1) & 0x7F;
+    return gray ? (uint32_t)gray[idx] : idx;
+  }
+  // bit i of the low byte of x -> bit 4i (byte-permute selector nibbles, one per pixel)
+  __device__ __forceinline__ static uint32_t sel_bits(uint32_t x) {
+    x &= 0xFFu;
+    x = (x | (x << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return (x | (x << 3)) & 0x11111111u;
+  }
+
+  // Pixels [xa, xb) of window row `row`.  Per 32-pixel coverage word the priority (R#13) is
+  // resolved on whole words into a 3-bit colour index per pixel (0 background, 1 playfield,
+  // 2 P0/M0, 3 P1/M1, 4 ball); per 16-pixel chunk the index bits become byte-permute selectors
+  // and four PRMTs pick the colour bytes.  Words outside the span are skipped (unrolled: every
+  // mask word is read with a constant index).
   __device__ __forceinline__ void render_span(const Masks& M, PixWriter& pw, uint32_t line, uint32_t row,
                                               uint32_t xa, uint32_t xb, const uint8_t* gray) {
-    const uint32_t cbk = shade(colubk, gray), c0 = shade(colup0, gray), c1 = shade(colup1, gray),
-                   cbl = shade(colupf, gray);
-    const uint32_t cpl = (ctrlpf & 2) ? c0 : cbl, cpr = (ctrlpf & 2) ? c1 : cbl;
-    const bool pfp = ctrlpf & 4;
+    const uint32_t gbk = shade1(colubk, gray), g0 = shade1(colup0, gray), g1 = shade1(colup1, gray),
+                   gbl = shade1(colupf, gray);
+    const bool score = (ctrlpf & 2) != 0, pfp = (ctrlpf & 4) != 0;
+    // permute source bytes: 0 background, 1 playfield (score mode: the player colour of the
+    // half), 2 P0/M0, 3 P1/M1, 4 ball (COLUPF)
+    const uint32_t hiw = (g0 << 16) | (g1 << 24);
+    const uint32_t Xl = gbk | ((score ? g0 : gbl) << 8) | hiw, Xr = gbk | ((score ? g1 : gbl) << 8) | hiw;
     const bool comb = (int32_t)line == comb_line;
-    for (uint32_t c = xa >> 4; c <= (xb - 1) >> 4; ++c) {
-      const int k = (int)(c >> 1);
-      const uint32_t hs = 16u * (c & 1u);
-      const uint32_t q0 = (M.p0[k] | M.m0[k]) >> hs, q1 = (M.p1[k] | M.m1[k]) >> hs;
-      const uint32_t qb = M.bl[k] >> hs, qp = M.pf[k] >> hs;
-      const uint32_t x0 = 16u * c;
-      const uint32_t cp = x0 < 80u ? cpl : cpr;
-      const bool pf_only = ((q0 | q1 | qb) & 0xFFFFu) == 0;
-      uint32_t px[4], bm[4];
+    const uint32_t c_lo = xa >> 4, c_hi = (xb - 1) >> 4;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        px[j] = pf_only ? (cbk ^ ((cbk ^ cp) & nib_bytes(qp >> (4 * j))))
-                        : group_px(q0, q1, qb, qp, 4u * j, pfp, c0, c1, cbl, cp, cbk);
-        bm[j] = (xa <= x0 && xb >= x0 + 16u) ? 0xFFFFFFFFu : group_mask(x0 + 4u * j, xa, xb);
+    for (int k = 0; k < 5; ++k) {
+      if (2u * k + 1u < c_lo || 2u * k > c_hi) continue;
+      const uint32_t a = M.p0[k] | M.m0[k], b = M.p1[k] | M.m1[k], l = M.bl[k], f = M.pf[k];
+      uint32_t e0, e1, eb, ep;
+      if (!pfp) {
+        e0 = a; e1 = b & ~a; eb = l & ~(a | b); ep = f & ~(a | b | l);
+      } else {
+        eb = l; ep = f & ~l; e0 = a & ~(l | f); e1 = b & ~(l | f | a);
       }
-      if (comb && c == 0) { px[0] = pw.fill; px[1] = pw.fill; }  // HMOVE comb, x < 8 (R#11)
-      pw.emit((int32_t)(row * 10u + c), px[0], px[1], px[2], px[3], bm[0], bm[1], bm[2], bm[3]);
+      const uint32_t i0 = ep | e1, i1 = e0 | e1, i2 = eb;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t c = 2u * k + h;
+        if (c < c_lo || c > c_hi) continue;
+        const uint32_t x0 = 16u * c, sh = 16u * h;
+        const uint32_t X = x0 < 80u ? Xl : Xr;
+        const uint32_t sa = sel_bits(i0 >> sh) | (sel_bits(i1 >> sh) << 1) | (sel_bits(i2 >> sh) << 2);
+        const uint32_t sb = sel_bits(i0 >> (sh + 8u)) | (sel_bits(i1 >> (sh + 8u)) << 1) | (sel_bits(i2 >> (sh + 8u)) << 2);
+        uint32_t p0 = __byte_perm(X, gbl, sa), p1 = __byte_perm(X, gbl, sa >> 16);
+        const uint32_t p2 = __byte_perm(X, gbl, sb), p3 = __byte_perm(X, gbl, sb >> 16);
+        if (comb && c == 0) { p0 = pw.fill; p1 = pw.fill; }  // HMOVE comb, x < 8 (R#11)
+        if (xa <= x0 && xb >= x0 + 16u) {
+          pw.emit_full((int32_t)(row * 10u + c), p0, p1, p2, p3);
+        } else {
+          const uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 16u ? xb - x0 : 16u;
+          const uint32_t r = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+          pw.emit((int32_t)(row * 10u + c), p0, p1, p2, p3, nib_bytes(r), nib_bytes(r >> 4), nib_bytes(r >> 8),
+                  nib_bytes(r >> 12));
+        }
+      }
     }
   }
   __device__ __forceinline__ static void render_black(PixWriter& pw, uint32_t row, uint32_t xa, uint32_t xb) {

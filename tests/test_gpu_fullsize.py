@@ -133,7 +133,7 @@ def test_cfg2_full_trajectory_and_windows(engine):
     assert n_track >= len(base) + 200 and n_done >= 256   # the resets overlap the base set a little
 
 
-@pytest.mark.parametrize("engine", ["simt", "jit", "vjit"])
+@pytest.mark.parametrize("engine", ["simt", "jit", "vjit", "wsvjit"])
 def test_cfg4_full_trajectory_and_windows(engine):
     N = 32768
     roms = [games.build_rom(n) for n in ("R1", "R2", "R3", "R4")]

@@ -14,19 +14,20 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.fixture(autouse=True, params=["simt", "scalar", "jit", "vjit"])
+@pytest.fixture(autouse=True, params=["simt", "scalar", "jit", "vjit", "wsvjit"])
 def engine(request, monkeypatch):
     """Every parity test runs on all four engines: the batched SIMT datapath, the scalar engine
     (one env per warp, record-driven interpreter, warp-cooperative TIA replay), the JIT
     engine (the scalar engine with the cartridge code translated to CUDA, csrc/jit.h) and the
     VJIT engine (one env per lane running the translated code, block-scheduled by warp vote,
-    csrc/vjit_kernels.cuh)."""
+    csrc/vjit_kernels.cuh) and its warp-specialized variant WSVJIT (producer warps emulate,
+    consumer warps render)."""
     monkeypatch.setenv("CULE_ENGINE", request.param)
     return request.param
 
 
 def skip_jit_debug(engine):
-    if engine in ("jit", "vjit"):
+    if engine in ("jit", "vjit", "wsvjit"):
         pytest.skip("debug-entry test: the translated engines' debug_exec runs an interpreter (tested as "
                     "'scalar' / 'simt')")
 
@@ -446,7 +447,7 @@ def test_idle_skip_is_exact(src, engine):
     """The exact idle-loop skip (cule_config.idle_skip; R#24) skips
     whole [timer read; branch back] poll iterations in closed form: observations, rewards,
     dones, counters and the full state stay bit-identical to the oracle, which never skips."""
-    if engine in ("jit", "vjit"):
+    if engine in ("jit", "vjit", "wsvjit"):
         pytest.skip("the translated engines have no idle-loop skip (cule_create rejects the combination)")
     import oracle
     from paper_1907_08467_b200 import Env
