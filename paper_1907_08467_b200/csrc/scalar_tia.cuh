@@ -359,8 +359,11 @@ __device__ __forceinline__ void chunk_px(const TiaP& t, const Words& w, uint32_t
     eb = l; ep = f & ~l; e0 = a & ~(l | f); e1 = b & ~(l | f | a);
   }
   const uint32_t i0 = ep | e1, i1 = e0 | e1, i2 = eb;
-  const uint32_t sa = Tia::sel_bits(i0) | (Tia::sel_bits(i1) << 1) | (Tia::sel_bits(i2) << 2);
-  const uint32_t sb = Tia::sel_bits(i0 >> 8) | (Tia::sel_bits(i1 >> 8) << 1) | (Tia::sel_bits(i2 >> 8) << 2);
+  uint32_t sa = Tia::sel_bits(i0), sb = Tia::sel_bits(i0 >> 8);
+  if ((i1 | i2) & 0xFFFFu) {  // (playfield-only chunks, the common case, need one index bit)
+    sa |= (Tia::sel_bits(i1) << 1) | (Tia::sel_bits(i2) << 2);
+    sb |= (Tia::sel_bits(i1 >> 8) << 1) | (Tia::sel_bits(i2 >> 8) << 2);
+  }
   x0w = __byte_perm(X, cbl, sa);
   x1w = __byte_perm(X, cbl, sa >> 16);
   x2w = __byte_perm(X, cbl, sb);

@@ -314,8 +314,11 @@ struct Tia {
         if (c < c_lo || c > c_hi) continue;
         const uint32_t x0 = 16u * c, sh = 16u * h;
         const uint32_t X = x0 < 80u ? Xl : Xr;
-        const uint32_t sa = sel_bits(i0 >> sh) | (sel_bits(i1 >> sh) << 1) | (sel_bits(i2 >> sh) << 2);
-        const uint32_t sb = sel_bits(i0 >> (sh + 8u)) | (sel_bits(i1 >> (sh + 8u)) << 1) | (sel_bits(i2 >> (sh + 8u)) << 2);
+        uint32_t sa = sel_bits(i0 >> sh), sb = sel_bits(i0 >> (sh + 8u));
+        if (((i1 | i2) >> sh) & 0xFFFFu) {  // (playfield-only chunks need one index bit)
+          sa |= (sel_bits(i1 >> sh) << 1) | (sel_bits(i2 >> sh) << 2);
+          sb |= (sel_bits(i1 >> (sh + 8u)) << 1) | (sel_bits(i2 >> (sh + 8u)) << 2);
+        }
         uint32_t p0 = __byte_perm(X, gbl, sa), p1 = __byte_perm(X, gbl, sa >> 16);
         const uint32_t p2 = __byte_perm(X, gbl, sb), p3 = __byte_perm(X, gbl, sb >> 16);
         if (comb && c == 0) { p0 = pw.fill; p1 = pw.fill; }  // HMOVE comb, x < 8 (R#11)
