@@ -78,6 +78,10 @@ typedef struct {
                                  cule_create; required for GRAY84 (gray LUT), ignored for RAW  */
   int32_t engine;             /* CULE_ENGINE_AUTO (default) or one of the engines below; the
                                  environment variable CULE_ENGINE (simt|scalar|jit|vjit|wsvjit) overrides */
+  int32_t tia_delays;         /* 1: delayed register effects (R#35):
+                                 PF0/PF1/PF2 written at visible pixel x take effect at the next
+                                 4-pixel playfield cell boundary 4*ceil(x/4), GRP0/GRP1 one colour
+                                 clock after the write; 0 (default): every write at its clock    */
 } cule_config;
 
 /* Engines (all compute the same results, bit for bit):

@@ -38,7 +38,7 @@ class OrcConfig(ctypes.Structure):
                 ("max_episode_frames", ctypes.c_int32), ("line_cap", ctypes.c_int32),
                 ("ystart", ctypes.c_int32), ("score_addr", ctypes.c_uint8),
                 ("term_addr", ctypes.c_uint8), ("term_mask", ctypes.c_uint8),
-                ("pad_", ctypes.c_uint8), ("seed", ctypes.c_uint64),
+                ("tia_delays", ctypes.c_uint8), ("seed", ctypes.c_uint64),
                 ("env_index_base", ctypes.c_int64)]
 
 
@@ -57,6 +57,9 @@ def lib():
         L.orc_run_frame.argtypes = [u8p, ctypes.c_size_t, u8p, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_int, u8p, ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(ctypes.c_int64)]
+        L.orc_run_frame_ex.argtypes = [u8p, ctypes.c_size_t, u8p, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, u8p, ctypes.POINTER(ctypes.c_int64),
+                                       ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
         L.orc_gray_lut.argtypes = [u8p, u8p]
         L.orc_area84.argtypes = [u8p, u8p]
         L.orc_splitmix64.argtypes = [ctypes.c_uint64]
@@ -107,14 +110,16 @@ def exec_instr(rom: bytes, state: np.ndarray, n: int = 1, line_cap: int = 1024):
 
 
 def run_frame(rom: bytes, state: np.ndarray, action: int = -1, ystart: int = 34,
-              line_cap: int = 1024, render: bool = True):
-    """Run one frame in place; returns (status, fb or None, instructions, scanlines)."""
+              line_cap: int = 1024, render: bool = True, tia_delays: int = 0):
+    """Run one frame in place; returns (status, fb or None, instructions, scanlines).
+    tia_delays=1: the delayed register effects of DESIGN.md R#35."""
     r = _rom_arr(rom)
     fb = np.zeros(FB_W * FB_H, np.uint8) if render else None
     ic = ctypes.c_int64(0)
     lines = ctypes.c_int64(0)
-    st = lib().orc_run_frame(_u8(r), len(r), _u8(state), action, ystart, line_cap,
-                             _u8(fb) if render else None, ctypes.byref(ic), ctypes.byref(lines))
+    st = lib().orc_run_frame_ex(_u8(r), len(r), _u8(state), action, ystart, line_cap,
+                                _u8(fb) if render else None, ctypes.byref(ic), ctypes.byref(lines),
+                                int(tia_delays))
     return st, (fb.reshape(FB_H, FB_W) if render else None), ic.value, lines.value
 
 

@@ -59,6 +59,7 @@ typedef struct {
   int ystart;
   uint8_t* fb;         /* 160x210 palette indices                                        */
   uint32_t last_lines; /* scanlines of the last completed frame (diagnostic)              */
+  int tia_delays;      /* delayed register effects [R#35] (opt-in; 0 = every write at T)   */
 } Machine;
 
 /* ---- snapshot layout --------------------------------------------------------- */
@@ -273,6 +274,16 @@ static void tia_write(Machine* m, int r, uint8_t v) {
   int line = (int)(T / 228);
   int h = (int)(T % 228);
   int hp = h - 68;
+  if (m->tia_delays) {
+    /* [R#35] a playfield register written at visible pixel x = h - 68 takes effect at the next
+     * 4-pixel playfield cell boundary, 4*ceil(x/4); GRP0/GRP1 one colour clock after the
+     * write; the TIA runs on with the old value until then (the clocks in between are drawn
+     * and collide with it), then the write lands */
+    if ((r == 0x0D || r == 0x0E || r == 0x0F) && hp > 0 && hp % 4 != 0)
+      tia_catch_up(m, T + (uint32_t)(4 - hp % 4));
+    else if (r == 0x1B || r == 0x1C)
+      tia_catch_up(m, T + 1u);
+  }
   switch (r) {
     case 0x00: { uint8_t nv = (v >> 1) & 1; if (!m->vsync && nv) m->vsync_rose = 1; m->vsync = nv; } break;
     case 0x01: m->vblank = (v >> 1) & 1; break;
@@ -906,11 +917,17 @@ int orc_exec(const uint8_t* rom, size_t rom_len, uint8_t* state, int n_instr, in
 
 int orc_run_frame(const uint8_t* rom, size_t rom_len, uint8_t* state, int action, int ystart,
                   int line_cap, uint8_t* fb, int64_t* instr_out, int64_t* lines_out) {
+  return orc_run_frame_ex(rom, rom_len, state, action, ystart, line_cap, fb, instr_out, lines_out, 0);
+}
+
+int orc_run_frame_ex(const uint8_t* rom, size_t rom_len, uint8_t* state, int action, int ystart,
+                     int line_cap, uint8_t* fb, int64_t* instr_out, int64_t* lines_out, int tia_delays) {
   if (!valid_rom_len(rom_len)) return -1;
   Machine m;
   memset(&m, 0, sizeof m);
   load_state(&m, state);
   bind(&m, rom, rom_len);
+  m.tia_delays = tia_delays;
   if (action >= 0) latch_inputs(&m, action);
   m.render = fb != NULL;
   m.ystart = ystart;
@@ -1051,6 +1068,7 @@ static int run_frames(orc_env* e, Machine* m, int nframes, int* rendered) {
     m->render = render;
     m->ystart = e->cfg.ystart;
     m->fb = fb;
+    m->tia_delays = e->cfg.tia_delays;
     m->episode_frames++;
     int r = run(m, e->cfg.line_cap, -1, NULL);
     m->render = 0;

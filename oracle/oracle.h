@@ -40,7 +40,7 @@ typedef struct {
   uint8_t score_addr;         /* RAM bus address of the BCD score high byte                */
   uint8_t term_addr;          /* done iff RAM[term_addr] & term_mask                        */
   uint8_t term_mask;
-  uint8_t pad_;
+  uint8_t tia_delays;         /* 1: delayed register effects [R#35] (default 0)              */
   uint64_t seed;              /* reset-cache construction seed                             */
   int64_t env_index_base;     /* global id of local env 0                                  */
 } orc_config;
@@ -58,6 +58,9 @@ int orc_exec(const uint8_t* rom, size_t rom_len, uint8_t* state, int n_instr, in
  * *instr_out gets the number of instructions executed. */
 int orc_run_frame(const uint8_t* rom, size_t rom_len, uint8_t* state, int action, int ystart,
                   int line_cap, uint8_t* fb, int64_t* instr_out, int64_t* lines_out);
+/* orc_run_frame with the delayed register effects of DESIGN.md R#35 on (tia_delays = 1) or off. */
+int orc_run_frame_ex(const uint8_t* rom, size_t rom_len, uint8_t* state, int action, int ystart,
+                     int line_cap, uint8_t* fb, int64_t* instr_out, int64_t* lines_out, int tia_delays);
 /* Gray LUT derived from an RGB palette (384 bytes) — §8(c).12 */
 void orc_gray_lut(const uint8_t* rgb, uint8_t* gray128);
 /* area84 of a 160x210 gray image (u8) — §8(c).12, exact area weights, round-half-even */

@@ -39,7 +39,7 @@ class CuleConfig(ctypes.Structure):
                 ("idle_skip", ctypes.c_uint8), ("seed", ctypes.c_uint64),
                 ("env_index_base", ctypes.c_int64),
                 ("palette_rgb", ctypes.POINTER(ctypes.c_uint8)),
-                ("engine", ctypes.c_int32)]
+                ("engine", ctypes.c_int32), ("tia_delays", ctypes.c_int32)]
 
 CULE_ENGINE_AUTO, CULE_ENGINE_SIMT, CULE_ENGINE_SCALAR, CULE_ENGINE_JIT, CULE_ENGINE_VJIT = 0, 1, 2, 3, 4
 CULE_ENGINE_WSVJIT = 5

@@ -18,13 +18,14 @@ enum Event : uint32_t { EV_NONE = 0, EV_LOGFULL = 1, EV_FRAME = 2, EV_FAULT = 3 
 // only, so no caller state is forced into local memory
 __device__ __noinline__ uint32_t flush_call(uint32_t* tw, uint32_t* pw, const uint32_t* lg, uint32_t s,
                                             uint32_t n, uint32_t fin, uint32_t t, uint32_t ystart,
-                                            const uint8_t* gray) {
-  flush_lane(tw, pw, lg, s, n, fin != 0, t, ystart, gray);
+                                            const uint8_t* gray, uint32_t delays) {
+  flush_lane(tw, pw, lg, s, n, fin != 0, t, ystart, gray, delays);
   return tw[7 * s] >> 16;  // collision latches
 }
 __device__ __forceinline__ uint32_t coll_read_flush(uint32_t* tw, uint32_t* pw, const uint32_t* lg, uint32_t s,
-                                                    uint32_t n, uint32_t t, uint32_t ystart, const uint8_t* gray) {
-  return flush_call(tw, pw, lg, s, n, 1u, t, ystart, gray);
+                                                    uint32_t n, uint32_t t, uint32_t ystart, const uint8_t* gray,
+                                                    uint32_t delays) {
+  return flush_call(tw, pw, lg, s, n, 1u, t, ystart, gray, delays);
 }
 
 struct Ctx {
@@ -41,6 +42,7 @@ struct Ctx {
   uint32_t ystart, line_cap;
   uint32_t cap_cycles;    // 76 * line_cap
   uint32_t idle_skip;     // exact idle-loop skip enabled (cule_config.idle_skip)
+  uint32_t tia_delays;    // delayed register effects (cule_config.tia_delays, R#35)
 };
 
 struct Cpu {
@@ -98,7 +100,7 @@ struct Cpu {
 
   // collision-latch read: flush this lane's log (divergent but rare) and advance to t
   __device__ __forceinline__ uint32_t tia_coll_read(const Ctx& c, uint32_t r, uint32_t t) {
-    const uint32_t coll = coll_read_flush(c.tw, c.pw, c.lg, c.s, log_len, t, c.ystart, c.gray);
+    const uint32_t coll = coll_read_flush(c.tw, c.pw, c.lg, c.s, log_len, t, c.ystart, c.gray, c.tia_delays);
     log_len = 0;
     return (((coll >> (2 * r)) & 1u) << 7) | (((coll >> (2 * r + 1)) & 1u) << 6);
   }

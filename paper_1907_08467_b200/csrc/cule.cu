@@ -209,6 +209,7 @@ static cule::Params base_params(const cule_env* e) {
   p.obs_stride = (uint32_t)obs_bytes_of(e->cfg.obs_mode);
   p.stacked = 0u;
   p.stack_slot = 0u;
+  p.tia_delays = e->cfg.tia_delays ? 1u : 0u;
   for (int r = 0; r < 4; ++r) { p.slot_start[r] = e->slot_start[r]; p.first_env[r] = e->first_env[r]; }
   return p;
 }
@@ -319,6 +320,7 @@ void cule_default_config(cule_config* c) {
   c->idle_skip = 0;
   c->palette_rgb = nullptr;
   c->engine = CULE_ENGINE_AUTO;
+  c->tia_delays = 0;
 }
 
 size_t cule_workspace_bytes(int num_envs, int n_roms, const cule_config* cfg) {

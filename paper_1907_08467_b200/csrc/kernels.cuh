@@ -72,6 +72,7 @@ struct Params {
   // env whose step ended the episode gets its new start observation in all four slots
   uint32_t obs_stride;
   uint32_t stacked, stack_slot;
+  uint32_t tia_delays;      // delayed register effects (cule_config.tia_delays; R#35)
 };
 
 // cartridge bank switching (F8 / F6 / F4; DESIGN.md §2 R#31, R#34): banks of ROM r, and the
@@ -172,6 +173,7 @@ __device__ __forceinline__ Ctx stage_block(const Params& p, uint8_t* smem, bool 
   c.line_cap = p.line_cap;
   c.cap_cycles = 76u * p.line_cap;
   c.idle_skip = p.idle_skip;
+  c.tia_delays = p.tia_delays;
   return c;
 }
 
@@ -330,7 +332,8 @@ __device__ __forceinline__ int32_t simulate(Cpu& m, const Ctx& c, bool active, u
     }
     if (__any_sync(kFull, ev != EV_NONE)) {
       const bool fin = ev == EV_FRAME || ev == EV_FAULT || ev == EV_BUDGET;
-      if (m.log_len || fin) flush_call(c.tw, c.pw, c.lg, c.s, m.log_len, fin ? 1u : 0u, 3u * m.fc, c.ystart, c.gray);
+      if (m.log_len || fin)
+        flush_call(c.tw, c.pw, c.lg, c.s, m.log_len, fin ? 1u : 0u, 3u * m.fc, c.ystart, c.gray, c.tia_delays);
       m.log_len = 0;
       if (ev == EV_FRAME) {
         end_frame(m, c);

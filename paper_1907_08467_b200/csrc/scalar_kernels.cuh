@@ -136,7 +136,8 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
                                               uint32_t* lg, uint32_t* tw, uint32_t cap_cycles, uint32_t lane,
                                               uint32_t nframes, uint8_t* frame_out, uint32_t& episode_frames,
                                               int32_t budget, uint32_t ystart, const uint8_t* gray,
-                                              uint32_t rec_s, uint8_t* obs84, uint8_t* ring, const uint8_t* cols) {
+                                              uint32_t rec_s, uint8_t* obs84, uint8_t* ring, const uint8_t* cols,
+                                              uint32_t tia_delays) {
   const uint32_t fill = kGray ? (uint32_t)gray[0] * 0x01010101u : 0u;
   RowBuf rb;
   rb.fill = fill;
@@ -185,7 +186,7 @@ __device__ __forceinline__ int32_t simulate_s(SMach* M, const uint8_t* rom_all, 
     const bool fin = ev == SE_FRAME || ev == SE_FAULT || ev == SE_BUDGET;
     const bool tgt = fin || ev == SE_COLL;
     const uint32_t target = fin ? 3u * M->fc : M->abort_T;
-    const uint32_t coll = flush_coop(tw, lg, n, tgt, target, rb, lane, ystart, gray);
+    const uint32_t coll = flush_coop(tw, lg, n, tgt, target, rb, lane, ystart, gray, tia_delays);
     if (lane == 0u) {
       M->log_len = 0u;
       M->coll = coll;
@@ -273,7 +274,7 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
   const int32_t status = simulate_s<kGray, kDebug>(M, rom_all, dtab, ram, lg, tw, 76u * p.line_cap, lane,
                                                    kDebug ? 1u : p.fs, frame_out, episode_frames, p.debug_instr,
                                                    p.ystart, gray, rec_s, obs84, wb + kSOffRing,
-                                                   smem + kSmCols);
+                                                   smem + kSmCols, p.tia_delays);
   if (kDebug) {
     if (lane == 0u) {
       if (status == RUN_JAM) M->fault = 1u;

@@ -438,7 +438,7 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
 // replay n entries of the warp's log, then (optionally) advance to t_final; returns collisions
 __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg, uint32_t n, bool fin,
                                                uint32_t t_final, RowBuf& rb, uint32_t lane, uint32_t ystart,
-                                               const uint8_t* gray) {
+                                               const uint8_t* gray, uint32_t delays) {
   TiaP t;
   t.load(tw);
   Words w{0u, 0u, 0u, 0u, 0u, 0u};
@@ -448,7 +448,7 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
   for (uint32_t k = 0; k < kend; ++k) {
     const uint32_t e = k < n ? lg[k] : (t_final << 14);
     const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
-    catch_up_coop(t, T, rb, lane, ystart, gray, w, dirty);
+    catch_up_coop(t, k < n ? effect_clock(T, r, delays) : T, rb, lane, ystart, gray, w, dirty);
     if (k == n) break;
     __syncwarp();  // reconverge: the register update is warp-uniform work, issued once
     t.apply(r, e & 0xFFu, T);

@@ -457,11 +457,25 @@ struct Tia {
   }
 };
 
+// Effect clock of a logged write at colour clock T (R#35, opt-in `delays`): a
+// playfield register written at visible pixel x lands at the next 4-pixel cell boundary
+// 4*ceil(x/4), GRP0/GRP1 one colour clock later; without delays, and for every other register,
+// T itself (R#4).  The replay catches the TIA up to the effect clock, then applies the write.
+__device__ __forceinline__ uint32_t effect_clock(uint32_t T, uint32_t r, uint32_t delays) {
+  if (!delays) return T;
+  if (r - 0x0Du < 3u) {
+    const uint32_t h = T % 228u;
+    const uint32_t d = h > 68u ? (h - 68u) & 3u : 0u;
+    return d ? T + 4u - d : T;
+  }
+  return (r - 0x1Bu < 2u) ? T + 1u : T;
+}
+
 // Replay n log entries of this lane, then (optionally) advance to t_final.
 // tw: this thread's TIA words, pw_w: pixel-writer words, lg: log words (all stride s).
 __device__ __forceinline__ void flush_lane(uint32_t* tw, uint32_t* pw_w, const uint32_t* lg, uint32_t s,
                                            uint32_t n, bool final_catch, uint32_t t_final, uint32_t ystart,
-                                           const uint8_t* gray) {
+                                           const uint8_t* gray, uint32_t delays = 0u) {
   Tia t;
   t.load(tw, s);
   PixWriter pw;
@@ -470,8 +484,9 @@ __device__ __forceinline__ void flush_lane(uint32_t* tw, uint32_t* pw_w, const u
   for (uint32_t k = 0; k < n; ++k) {
     uint32_t e = lg[k * s];
     uint32_t T = e >> 14;
-    t.catch_up(T, render, pw, ystart, gray);
-    t.apply((e >> 8) & 0x3Fu, e & 0xFFu, T);
+    const uint32_t r = (e >> 8) & 0x3Fu;
+    t.catch_up(effect_clock(T, r, delays), render, pw, ystart, gray);
+    t.apply(r, e & 0xFFu, T);
   }
   if (final_catch) t.catch_up(t_final, render, pw, ystart, gray);
   t.store(tw, s);

@@ -159,7 +159,7 @@ __device__ __forceinline__ int32_t simulate_v(SMach* M, uint32_t* tw, uint32_t* 
       const bool fin = ev == SE_FRAME || ev == SE_FAULT;
       const bool tgt = fin || ev == SE_COLL;
       const uint32_t target = fin ? 3u * M->fc : M->abort_T;
-      if (n || tgt) flush_lane(tw, pw, lg, 1u, n, tgt, target, p.ystart, gray);
+      if (n || tgt) flush_lane(tw, pw, lg, 1u, n, tgt, target, p.ystart, gray, p.tia_delays);
       const uint32_t coll = tw[7] >> 16;
       M->log_len = 0u;
       M->coll = coll;
@@ -453,7 +453,7 @@ __device__ __forceinline__ void wsvjit_kernel_body(const Params& p) {
         const uint32_t n = m0 & 0xFFu, ev = m0 >> 8;
         const bool fin = ev == SE_FRAME || ev == SE_FAULT;
         const bool tg = fin || ev == SE_COLL;
-        if (n || tg) flush_lane(tw, pw, lw + (buf ? kWOffL1 : kWOffL0), 1u, n, tg, T, p.ystart, gray);
+        if (n || tg) flush_lane(tw, pw, lw + (buf ? kWOffL1 : kWOffL0), 1u, n, tg, T, p.ystart, gray, p.tia_delays);
         if (ev == SE_FRAME) {
           end_frame_tia(tw, T / 228u);
           if (render) pw_end(pw, 1u);

@@ -459,3 +459,32 @@ def test_idle_skip_is_exact(src, engine):
     check_engine(gpu)
     ref = oracle.OracleEnv(roms, n, 4, H.palette_rgb(), reset_cache_size=4)
     run_parity(gpu, ref, 30, seed=77)
+
+
+# ---- delayed register effects (opt-in; R#35) -----------------
+def _delay_programs():
+    # mid-line PF1 and GRP0 writes at every residue of the playfield cell (x = 6k - 26 on row 0;
+    # tests/test_oracle_delays.py pins the frames), plus a collision read of the result
+    out = []
+    for k in (8, 10, 12):
+        row0 = "    NOP\n" * k + "    LDA #$FF\n    STA $0E\n" + "    NOP\n" * 2 + "    LDA #$00\n    STA $1B\n"
+        out.append(micro.static_frame(pokes=[(0x09, 0x1E), (0x08, 0x44), (0x06, 0x86), (0x1B, 0xFF), (0x0E, 0x00)],
+                                      positions=[(0x10, 16)], kernel_row0=row0, store_collisions=True))
+    return out
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_tia_delays_static_frames_raw(case):
+    """Static frames with mid-line playfield and GRP writes, RAW frames every step, with the
+    delayed register effects on: frames, collision latches and state equal the oracle's."""
+    rom = micro.build(_delay_programs()[case])
+    gpu, ref = pair([rom], 8, 1, "raw", reset_cache_size=2, startup_frames=4, max_random_frames=3,
+                    tia_delays=1)
+    run_parity(gpu, ref, 6)
+
+
+def test_tia_delays_games_gray84():
+    """The four game ROMs (mid-line PF and GRP writes every line) with the delays on."""
+    roms = [games.build_rom(n) for n in ("R1", "R2", "R3", "R4")]
+    gpu, ref = pair(roms, 70, 4, reset_cache_size=4, tia_delays=1)
+    run_parity(gpu, ref, 16, check_every=5)
