@@ -60,6 +60,9 @@ typedef struct {
   uint8_t* fb;         /* 160x210 palette indices                                        */
   uint32_t last_lines; /* scanlines of the last completed frame (diagnostic)              */
   int tia_delays;      /* delayed register effects [R#35] (opt-in; 0 = every write at T)   */
+  uint8_t res_delay;   /* [R#36] objects reset during the visible part of line res_line (bits
+                          0 P0, 1 P1, 2 M0, 3 M1): their first copy is not drawn on that line */
+  int res_line;
 } Machine;
 
 /* ---- snapshot layout --------------------------------------------------------- */
@@ -91,6 +94,8 @@ static void save_state(const Machine* m, uint8_t* s) {
   s[52] = m->vdelp1; s[53] = m->vdelbl; s[54] = m->resmp0; s[55] = m->resmp1;
   s[56] = m->posP0; s[57] = m->posP1; s[58] = m->posM0; s[59] = m->posM1; s[60] = m->posBL;
   s[61] = m->rom_id; s[62] = m->fault;
+  /* [R#36] byte 63: the start-delay bits, when they apply to the line the TIA is on */
+  s[63] = (m->res_delay && m->res_line == (int)(m->t_tia / 228)) ? m->res_delay : 0;
   memcpy(s + 64, m->ram, 128);
   put32(s + 192, m->episode_frames);
   put32(s + 196, m->episode_index);
@@ -126,6 +131,8 @@ static void load_state(Machine* m, const uint8_t* s) {
   m->now = m->fc;
   m->wsync_req = 0;
   m->vsync_rose = 0;
+  m->res_delay = s[63] & 0x0F;
+  m->res_line = (int)(m->t_tia / 228);
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -167,26 +174,26 @@ static uint8_t reverse8(uint8_t g) {
 }
 
 static int cover_player(int x, uint8_t pos, uint8_t nusiz, uint8_t grp_new, uint8_t grp_old,
-                        uint8_t vdel, uint8_t refl) {
+                        uint8_t vdel, uint8_t refl, int skip_first) {
   uint8_t g = vdel ? grp_old : grp_new;
   if (refl) g = reverse8(g);
   int mode = nusiz & 7, off[3];
   int n = nusiz_offsets(mode, off);
   int scale = nusiz_scale(mode);
-  for (int k = 0; k < n; k++) {
+  for (int k = skip_first ? 1 : 0; k < n; k++) {
     int d = mod160(x - pos - off[k]);
     if (d < 8 * scale && ((g >> (7 - d / scale)) & 1)) return 1;
   }
   return 0;
 }
 
-static int cover_missile(int x, uint8_t pos, uint8_t nusiz, uint8_t enam, uint8_t resmp) {
+static int cover_missile(int x, uint8_t pos, uint8_t nusiz, uint8_t enam, uint8_t resmp, int skip_first) {
   if (!enam || resmp) return 0;
   int width = 1 << ((nusiz >> 4) & 3);
   int mode = nusiz & 7, off[3], n;
   if (mode == 5 || mode == 7) { off[0] = 0; n = 1; }
   else n = nusiz_offsets(mode, off);
-  for (int k = 0; k < n; k++)
+  for (int k = skip_first ? 1 : 0; k < n; k++)
     if (mod160(x - pos - off[k]) < width) return 1;
   return 0;
 }
@@ -205,10 +212,12 @@ static void tia_clock(Machine* m, int line, int x) {
     if (in_window) m->fb[(line - m->ystart) * ORC_FB_W + x] = 0;
     return; /* no collisions under VBLANK [R#12] */
   }
-  int p0 = cover_player(x, m->posP0, m->nusiz0, m->grp0new, m->grp0old, m->vdelp0, m->refp0);
-  int p1 = cover_player(x, m->posP1, m->nusiz1, m->grp1new, m->grp1old, m->vdelp1, m->refp1);
-  int m0 = cover_missile(x, m->posM0, m->nusiz0, m->enam0, m->resmp0);
-  int m1 = cover_missile(x, m->posM1, m->nusiz1, m->enam1, m->resmp1);
+  /* [R#36] the first copy of an object reset during the visible part of this line is not drawn */
+  int rd = (m->res_delay && line == m->res_line) ? m->res_delay : 0;
+  int p0 = cover_player(x, m->posP0, m->nusiz0, m->grp0new, m->grp0old, m->vdelp0, m->refp0, rd & 1);
+  int p1 = cover_player(x, m->posP1, m->nusiz1, m->grp1new, m->grp1old, m->vdelp1, m->refp1, rd & 2);
+  int m0 = cover_missile(x, m->posM0, m->nusiz0, m->enam0, m->resmp0, rd & 4);
+  int m1 = cover_missile(x, m->posM1, m->nusiz1, m->enam1, m->resmp1, rd & 8);
   int bl = cover_ball(m, x);
   int pf = cover_pf(m, x);
   /* collision latches, bit 2r = d7 and bit 2r+1 = d6 of read register r */
@@ -342,6 +351,11 @@ static void tia_write(Machine* m, int r, uint8_t v) {
     case 0x2B: m->hmp0 = m->hmp1 = m->hmm0 = m->hmm1 = m->hmbl = 0; break;
     case 0x2C: m->coll = 0; break;
     default: break; /* audio and $2D-$3F ignored */
+  }
+  if (m->tia_delays && r >= 0x10 && r <= 0x13 && hp >= 0) { /* [R#36] RESxx start delay */
+    if (m->res_line != line) m->res_delay = 0;
+    m->res_delay |= (uint8_t)(1u << (r - 0x10));
+    m->res_line = line;
   }
 }
 
@@ -805,6 +819,7 @@ static void end_frame(Machine* m) {
   m->fc -= 76 * L;
   m->timer_w -= (int32_t)(76 * L);
   m->t_tia -= 228 * L;
+  m->res_line -= (int)L;
   int cl = (int)m->comb_line - (int)L;
   m->comb_line = (int16_t)(cl < 0 ? -1 : cl);
   /* canonical timer stamp (§8(c).5) */
@@ -1080,6 +1095,7 @@ static int run_frames(orc_env* e, Machine* m, int nframes, int* rendered) {
 
 static void copy_machine_part(uint8_t* dst, const uint8_t* src) {
   memcpy(dst, src, 61);           /* CPU, clock, timer, inputs, TIA, positions */
+  dst[63] = src[63];              /* RESxx start-delay bits [R#36] */
   memcpy(dst + 64, src + 64, 128); /* RAM */
 }
 

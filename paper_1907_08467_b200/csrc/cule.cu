@@ -733,6 +733,7 @@ static int validate_snapshot(const cule_env* e, const uint8_t* s, size_t i) {
   const uint32_t fc = (uint32_t)s[8] | ((uint32_t)s[9] << 8) | ((uint32_t)s[10] << 16) | ((uint32_t)s[11] << 24);
   if (fc >= 76u * (uint32_t)e->cfg.line_cap) return fail(CULE_E_INVAL, at + "fc beyond the line cap");
   if (s[62] > 2) return fail(CULE_E_INVAL, at + "fault code not in {0,1,2}");
+  if (s[63] > 15) return fail(CULE_E_INVAL, at + "start-delay bits (byte 63) not in [0, 15]");
   return CULE_OK;
 }
 

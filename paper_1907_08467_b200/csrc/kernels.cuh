@@ -215,7 +215,7 @@ __device__ __forceinline__ void load_machine(Cpu& m, const Ctx& c, const Hdr& h,
   w[s] = pk(hb(h, 35), hb(h, 36), hb(h, 37), hb(h, 32));                // pf0 pf1 pf2 ctrlpf
   w[2 * s] = pk(hb(h, 26), hb(h, 27), hb(h, 38), hb(h, 39));            // nusiz0 nusiz1 grp0n grp0o
   w[3 * s] = pk(hb(h, 40), hb(h, 41), hb(h, 46), hb(h, 47));            // grp1n grp1o hmp0 hmp1
-  w[4 * s] = pk(hb(h, 48), hb(h, 49), hb(h, 50), 0);                    // hmm0 hmm1 hmbl
+  w[4 * s] = pk(hb(h, 48), hb(h, 49), hb(h, 50), hb(h, 63) & 0x0Fu);     // hmm0 hmm1 hmbl, start delay (R#36)
   const uint32_t flags = (hb(h, 25) & 1u) | ((hb(h, 33) & 1u) << 1) | ((hb(h, 34) & 1u) << 2) |
                          ((hb(h, 42) & 1u) << 3) | ((hb(h, 43) & 1u) << 4) | ((hb(h, 44) & 1u) << 5) |
                          ((hb(h, 45) & 1u) << 6) | ((hb(h, 51) & 1u) << 7) | ((hb(h, 52) & 1u) << 8) |
@@ -241,7 +241,7 @@ __device__ __forceinline__ Hdr pack_machine(const Cpu& m, const Ctx& c, uint32_t
   h.c[2] = make_uint4(pk(w1 >> 24, F(1), F(2), w1), pk(w1 >> 8, w1 >> 16, w2 >> 16, w2 >> 24),
                       pk(w3, w3 >> 8, F(3), F(4)), pk(F(5), F(6), w3 >> 16, w3 >> 24));
   h.c[3] = make_uint4(pk(w4, w4 >> 8, w4 >> 16, F(7)), pk(F(8), F(9), F(10), F(11)), w6,
-                      pk(w7, rom_id, m.fault, 0));
+                      pk(w7, rom_id, m.fault, (w4 >> 24) & 0x0Fu));
   return h;
 }
 
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(128, CULE_MINB) step_kernel(Params p) {
 #pragma unroll
       for (int q = 0; q < 12; ++q) {
         uint4 v = src[q];
-        if (q == 3) v.w = (v.w & 0x000000FFu) | (rom_id << 8);
+        if (q == 3) v.w = (v.w & 0xFF0000FFu) | (rom_id << 8);  // rom_id, fault 0, byte 63 kept (R#36)
         st[q * N + i] = v;
       }
       st[12 * N + i] = make_uint4(0u, e, 0u, (uint32_t)p.cache_score[ent]);
@@ -598,7 +598,7 @@ __global__ void reset_kernel(Params p, uint32_t obs_bytes, uint8_t* d_obs, const
   const uint4* c = reinterpret_cast<const uint4*>(p.cache_state + (size_t)ent * 256u);
   for (int q = 0; q < 12; ++q) {
     uint4 v = c[q];
-    if (q == 3) v.w = (v.w & 0x000000FFu) | (rom_id << 8);
+    if (q == 3) v.w = (v.w & 0xFF0000FFu) | (rom_id << 8);  // rom_id, fault 0, byte 63 kept (R#36)
     st[q * N + i] = v;
   }
   st[12 * N + i] = make_uint4(0u, 0u, 0u, (uint32_t)p.cache_score[ent]);
@@ -624,7 +624,7 @@ __global__ void unpack_kernel(uint8_t* state, const uint8_t* packed, uint32_t N)
   if (t >= (size_t)N * 16u) return;
   const size_t i = t >> 4, k = t & 15u;
   uint4 v = reinterpret_cast<const uint4*>(packed)[i * 16u + k];
-  if (k == 3) v.w &= 0x00FFFFFFu;          // byte 63 reserved
+  if (k == 3) v.w &= 0x0FFFFFFFu;          // byte 63: RESxx start-delay bits 0-3 (R#36)
   if (k == 12) v.w &= 0x0000FFFFu;         // bytes 206-207 reserved
   if (k >= 13) v = make_uint4(0, 0, 0, 0); // bytes 208-255 reserved
   reinterpret_cast<uint4*>(state)[k * N + i] = v;

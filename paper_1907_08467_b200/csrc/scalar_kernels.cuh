@@ -70,7 +70,7 @@ __device__ __forceinline__ void load_smach(SMach* M, const Hdr& h, const Params&
   tw[1] = pk(hb(h, 35), hb(h, 36), hb(h, 37), hb(h, 32));
   tw[2] = pk(hb(h, 26), hb(h, 27), hb(h, 38), hb(h, 39));
   tw[3] = pk(hb(h, 40), hb(h, 41), hb(h, 46), hb(h, 47));
-  tw[4] = pk(hb(h, 48), hb(h, 49), hb(h, 50), 0);
+  tw[4] = pk(hb(h, 48), hb(h, 49), hb(h, 50), hb(h, 63) & 0x0Fu);  // + RESxx start delay (R#36)
   const uint32_t flags = (hb(h, 25) & 1u) | ((hb(h, 33) & 1u) << 1) | ((hb(h, 34) & 1u) << 2) |
                          ((hb(h, 42) & 1u) << 3) | ((hb(h, 43) & 1u) << 4) | ((hb(h, 44) & 1u) << 5) |
                          ((hb(h, 45) & 1u) << 6) | ((hb(h, 51) & 1u) << 7) | ((hb(h, 52) & 1u) << 8) |
@@ -94,7 +94,7 @@ __device__ __forceinline__ Hdr pack_smach(const SMach* M, const uint32_t* tw, ui
   h.c[2] = make_uint4(pk(w1 >> 24, F(1), F(2), w1), pk(w1 >> 8, w1 >> 16, w2 >> 16, w2 >> 24),
                       pk(w3, w3 >> 8, F(3), F(4)), pk(F(5), F(6), w3 >> 16, w3 >> 24));
   h.c[3] = make_uint4(pk(w4, w4 >> 8, w4 >> 16, F(7)), pk(F(8), F(9), F(10), F(11)), w6,
-                      pk(w7, rom_id, M->fault, 0));
+                      pk(w7, rom_id, M->fault, (w4 >> 24) & 0x0Fu));
   return h;
 }
 
@@ -327,7 +327,7 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
     if (lane == 12u) v = reinterpret_cast<const uint4*>(stg)[4];
     else if (done) {
       v = reinterpret_cast<const uint4*>(p.cache_state + (size_t)ent * 256u)[lane];
-      if (lane == 3u) v.w = (v.w & 0x000000FFu) | (rom_id << 8);
+      if (lane == 3u) v.w = (v.w & 0xFF0000FFu) | (rom_id << 8);  // byte 63 kept (R#36)
     } else {
       v = lane < 4u ? reinterpret_cast<const uint4*>(stg)[lane] : reinterpret_cast<const uint4*>(ram)[lane - 4u];
     }

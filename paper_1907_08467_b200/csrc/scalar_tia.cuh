@@ -90,7 +90,7 @@ struct TiaP {
   __device__ __forceinline__ uint32_t open_pairs() const { return kPairTable.v[pres] & ~coll(); }
 
   // apply a logged write at colour clock T (DESIGN.md §2 R#7-R#12)
-  __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T) {
+  __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T, uint32_t delays) {
     switch (r) {
       case 0x01: setf(0, v >> 1); break;
       case 0x04: w2 = with_byte(w2, 0, v); break;
@@ -106,6 +106,8 @@ struct TiaP {
         const uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
         if (r == 0x14u) w7 = with_byte(w7, 0, p);
         else w6 = with_byte(w6, (int)(r - 0x10u), p);
+        // RESxx start delay (R#36): w4 byte 3, bits 0 P0 .. 3 M1, for the rest of this line
+        if (delays && hp >= 0 && r != 0x14u) w4 |= 1u << (24u + (r - 0x10u));
       } break;
       case 0x1B:  // GRP0; GRP1 old <- new
         w2 = with_byte(w2, 2, v); w3 = with_byte(w3, 1, byte_of(w3, 0));
@@ -195,12 +197,12 @@ __device__ __forceinline__ void update_words(const TiaP& t, uint32_t k, Words& w
       q = mode == 5u ? spread2(q) : (mode == 7u ? spread4(q) : q);
       pat = g ? q : 0u;
       pos = byte_of(t.w6, (int)idx);
-      cps = Tia::copies(mode);
+      cps = Tia::copies(mode) & ~((t.w4 >> (24u + o)) & 1u);  // RESxx start delay (R#36)
     } else if (o < 4u) { // missiles: enabled and not locked to the player; one copy in modes 5/7
       const bool en = t.f(3 + (int)idx) && !t.f(10 + (int)idx);
       pat = en ? (1u << (1u << ((nusiz >> 4) & 3u))) - 1u : 0u;
       pos = byte_of(t.w6, 2 + (int)idx);
-      cps = (mode == 5u || mode == 7u) ? 1u : Tia::copies(mode);
+      cps = ((mode == 5u || mode == 7u) ? 1u : Tia::copies(mode)) & ~((t.w4 >> (24u + o)) & 1u);
     } else {             // ball
       pat = t.ball_on() ? (1u << (1u << ((byte_of(t.w1, 3) >> 4) & 3u))) - 1u : 0u;
       pos = byte_of(t.w7, 0);
@@ -443,20 +445,34 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
   t.load(tw);
   Words w{0u, 0u, 0u, 0u, 0u, 0u};
   uint32_t dirty = 0x3Fu;
-  // entries 0..n-1, then (fin) the final catch-up to t_final: one catch_up_coop call site
+  // entries 0..n-1 (catch up to the write's effect clock, then apply it), then (fin) the final
+  // catch-up to t_final; a RESxx start delay ends with its line: the catch-up stops there first
+  // (one catch_up_coop call site)
   const uint32_t kend = fin ? n + 1u : n;
-  for (uint32_t k = 0; k < kend; ++k) {
+  for (uint32_t k = 0; k < kend;) {
     const uint32_t e = k < n ? lg[k] : (t_final << 14);
     const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
-    catch_up_coop(t, k < n ? effect_clock(T, r, delays) : T, rb, lane, ystart, gray, w, dirty);
+    uint32_t to = k < n ? effect_clock(T, r, delays) : T;
+    bool line_end = false;
+    if (t.w4 >> 24) {
+      const uint32_t le = (t.t / 228u + 1u) * 228u;
+      if (to >= le) { to = le; line_end = true; }
+    }
+    catch_up_coop(t, to, rb, lane, ystart, gray, w, dirty);
+    if (line_end) {  // the delayed first copies show again from the next line
+      dirty |= t.w4 >> 24;
+      t.w4 &= 0x00FFFFFFu;
+      continue;
+    }
     if (k == n) break;
     __syncwarp();  // reconverge: the register update is warp-uniform work, issued once
-    t.apply(r, e & 0xFFu, T);
+    t.apply(r, e & 0xFFu, T, delays);
     if (r - 6u < 4u) {  // COLUxx: refresh the shaded colour, ordered before any lane's next read
       shade_store(rb.ring_s + kShadeOff + 4u * (r - 6u), e & 0xFFu, gray);
       __syncwarp();
     }
     dirty |= kDirtyTable.v[r];
+    ++k;
   }
   __syncwarp();
   if (lane == 0u) t.store(tw);

@@ -133,6 +133,8 @@ struct Tia {
   uint32_t posP0, posP1, posM0, posM1, posBL;
   uint32_t coll;
   uint32_t t_tia;
+  uint32_t rdel;  // RESxx start delay (R#36): bits 0 P0, 1 P1, 2 M0, 3 M1 reset during the visible
+                  // part of the line t_tia is on; their first copy is not drawn until it ends
 
   __device__ __forceinline__ uint32_t f(int b) const { return (flags >> b) & 1u; }
   __device__ __forceinline__ void setf(int b, uint32_t v) { flags = (flags & ~(1u << b)) | ((v & 1u) << b); }
@@ -144,7 +146,7 @@ struct Tia {
     pf0 = b & 0xFF; pf1 = (b >> 8) & 0xFF; pf2 = (b >> 16) & 0xFF; ctrlpf = b >> 24;
     nusiz0 = c & 0xFF; nusiz1 = (c >> 8) & 0xFF; grp0n = (c >> 16) & 0xFF; grp0o = c >> 24;
     grp1n = d & 0xFF; grp1o = (d >> 8) & 0xFF; hmp0 = (d >> 16) & 0xFF; hmp1 = d >> 24;
-    hmm0 = e & 0xFF; hmm1 = (e >> 8) & 0xFF; hmbl = (e >> 16) & 0xFF;
+    hmm0 = e & 0xFF; hmm1 = (e >> 8) & 0xFF; hmbl = (e >> 16) & 0xFF; rdel = e >> 24;
     flags = g & 0xFFFF; comb_line = (int32_t)(int16_t)(g >> 16);
     posP0 = h & 0xFF; posP1 = (h >> 8) & 0xFF; posM0 = (h >> 16) & 0xFF; posM1 = h >> 24;
     posBL = k & 0xFF; coll = k >> 16;
@@ -155,7 +157,7 @@ struct Tia {
     w[s] = pf0 | (pf1 << 8) | (pf2 << 16) | (ctrlpf << 24);
     w[2 * s] = nusiz0 | (nusiz1 << 8) | (grp0n << 16) | (grp0o << 24);
     w[3 * s] = grp1n | (grp1o << 8) | (hmp0 << 16) | (hmp1 << 24);
-    w[4 * s] = hmm0 | (hmm1 << 8) | (hmbl << 16);
+    w[4 * s] = hmm0 | (hmm1 << 8) | (hmbl << 16) | (rdel << 24);
     w[5 * s] = (flags & 0xFFFF) | ((uint32_t)(comb_line & 0xFFFF) << 16);
     w[6 * s] = posP0 | (posP1 << 8) | (posM0 << 16) | (posM1 << 24);
     w[7 * s] = posBL | (coll << 16);
@@ -192,27 +194,29 @@ struct Tia {
         m.place(pat, p >= 160u ? p - 160u : p);
       }
   }
-  __device__ __forceinline__ static void player_mask(W5& m, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl) {
+  __device__ __forceinline__ static void player_mask(W5& m, uint32_t pos, uint32_t nusiz, uint32_t g, uint32_t refl,
+                                                     uint32_t skip_first) {
     m.zero();
     if (g == 0) return;
     const uint32_t mode = nusiz & 7;
     uint32_t pat = refl ? g : rev8(g);  // pixel d shows graphic bit 7-d (bit d when reflected)
     if (mode == 5) pat = spread2(pat);
     else if (mode == 7) pat = spread4(pat);
-    place_copies(m, pat, pos, copies(mode));
+    place_copies(m, pat, pos, copies(mode) & ~skip_first);
   }
-  __device__ __forceinline__ static void missile_mask(W5& m, uint32_t pos, uint32_t nusiz, bool en) {
+  __device__ __forceinline__ static void missile_mask(W5& m, uint32_t pos, uint32_t nusiz, bool en,
+                                                      uint32_t skip_first) {
     m.zero();
     if (!en) return;
     const uint32_t mode = nusiz & 7;
     const uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3))) - 1u;
-    place_copies(m, pat, pos, (mode == 5 || mode == 7) ? 1u : copies(mode));
+    place_copies(m, pat, pos, ((mode == 5 || mode == 7) ? 1u : copies(mode)) & ~skip_first);
   }
   __device__ __forceinline__ void build_masks(Masks& M) const {
-    player_mask(M.p0, posP0, nusiz0, f(7) ? grp0o : grp0n, f(1));
-    player_mask(M.p1, posP1, nusiz1, f(8) ? grp1o : grp1n, f(2));
-    missile_mask(M.m0, posM0, nusiz0, f(3) && !f(10));
-    missile_mask(M.m1, posM1, nusiz1, f(4) && !f(11));
+    player_mask(M.p0, posP0, nusiz0, f(7) ? grp0o : grp0n, f(1), rdel & 1u);
+    player_mask(M.p1, posP1, nusiz1, f(8) ? grp1o : grp1n, f(2), (rdel >> 1) & 1u);
+    missile_mask(M.m0, posM0, nusiz0, f(3) && !f(10), (rdel >> 2) & 1u);
+    missile_mask(M.m1, posM1, nusiz1, f(4) && !f(11), (rdel >> 3) & 1u);
     M.bl.zero();
     if (f(9) ? f(6) : f(5)) M.bl.place((1u << (1u << ((ctrlpf >> 4) & 3))) - 1u, posBL);
     // playfield: 20 cells per half (PF0 D4-D7, PF1 D7-D0, PF2 D0-D7), each 4 pixels wide
@@ -395,7 +399,7 @@ struct Tia {
   }
 
   // apply a logged write at colour clock T (WSYNC/VSYNC/RSYNC/audio never reach the log)
-  __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T) {
+  __device__ __forceinline__ void apply(uint32_t r, uint32_t v, uint32_t T, uint32_t delays = 0u) {
     uint32_t line = T / 228u, h = T - line * 228u;
     int32_t hp = (int32_t)h - 68;
     switch (r) {
@@ -417,6 +421,7 @@ struct Tia {
         uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
         if (r == 0x10) posP0 = p; else if (r == 0x11) posP1 = p;
         else if (r == 0x12) posM0 = p; else if (r == 0x13) posM1 = p; else posBL = p;
+        if (delays && hp >= 0 && r != 0x14) rdel |= 1u << (r - 0x10);  // RESxx start delay (R#36)
       } break;
       case 0x1B: grp0n = v; grp1o = grp1n; break;
       case 0x1C: grp1n = v; grp0o = grp0n; setf(6, f(5)); break;
@@ -481,14 +486,25 @@ __device__ __forceinline__ void flush_lane(uint32_t* tw, uint32_t* pw_w, const u
   PixWriter pw;
   const bool render = pw_rendering(pw_w, s);
   if (render) pw.load(pw_w, s);
-  for (uint32_t k = 0; k < n; ++k) {
-    uint32_t e = lg[k * s];
-    uint32_t T = e >> 14;
-    const uint32_t r = (e >> 8) & 0x3Fu;
-    t.catch_up(effect_clock(T, r, delays), render, pw, ystart, gray);
-    t.apply(r, e & 0xFFu, T);
+  // entries 0..n-1 (catch up to the write's effect clock, then apply it), then the final
+  // catch-up; a RESxx start delay ends with its line: the catch-up stops there first (one
+  // catch_up call site keeps the replay code small)
+  const uint32_t kend = final_catch ? n + 1u : n;
+  for (uint32_t k = 0; k < kend;) {
+    const uint32_t e = k < n ? lg[k * s] : 0u;
+    const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
+    uint32_t to = k < n ? effect_clock(T, r, delays) : t_final;
+    bool line_end = false;
+    if (t.rdel) {
+      const uint32_t le = (t.t_tia / 228u + 1u) * 228u;
+      if (to >= le) { to = le; line_end = true; }
+    }
+    t.catch_up(to, render, pw, ystart, gray);
+    if (line_end) { t.rdel = 0u; continue; }
+    if (k == n) break;
+    t.apply(r, e & 0xFFu, T, delays);
+    ++k;
   }
-  if (final_catch) t.catch_up(t_final, render, pw, ystart, gray);
   t.store(tw, s);
   if (render) pw.save(pw_w, s);
 }

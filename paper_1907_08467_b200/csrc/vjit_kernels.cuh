@@ -253,7 +253,7 @@ __device__ __forceinline__ void vjit_kernel_body(const Params& p) {
 #pragma unroll
       for (int q = 0; q < 12; ++q) {
         uint4 v = src[q];
-        if (q == 3) v.w = (v.w & 0x000000FFu) | (rom_id << 8);
+        if (q == 3) v.w = (v.w & 0xFF0000FFu) | (rom_id << 8);  // rom_id, fault 0, byte 63 kept (R#36)
         st[q * N + i] = v;
       }
       st[12 * N + i] = make_uint4(0u, e, 0u, (uint32_t)p.cache_score[ent]);
@@ -501,7 +501,7 @@ __device__ __forceinline__ void wsvjit_kernel_body(const Params& p) {
 #pragma unroll
         for (int q = 0; q < 12; ++q) {
           uint4 v = src[q];
-          if (q == 3) v.w = (v.w & 0x000000FFu) | (rom_id << 8);
+          if (q == 3) v.w = (v.w & 0xFF0000FFu) | (rom_id << 8);  // rom_id, fault 0, byte 63 kept (R#36)
           st[q * N + i] = v;
         }
         st[12 * N + i] = make_uint4(0u, e, 0u, (uint32_t)p.cache_score[ent]);

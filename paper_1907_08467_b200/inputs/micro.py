@@ -726,3 +726,38 @@ Tab: .byte $5A
     .word Reset
     .word Reset
 """
+
+
+# ---------------------------------------------------------------------------------------------
+# M23 resp_at_vsync: a visible RESP0 right before the VSYNC write on the same line, so a RESxx
+# start delay (DESIGN.md R#36) is pending at the frame boundary.  After `STA WSYNC`: LDA #2 (2),
+# 20 NOPs (40), STA RESP0 ends at cycle 45 (hp = 67, player at 72), STA VSYNC at cycle 48
+# (colour clock 144, pixel 76): pixels 76..79 of the player fall on the next frame's line 0.
+# ---------------------------------------------------------------------------------------------
+def m23_resp_at_vsync() -> str:
+    return _HEAD + """
+Frame:
+    LDA #0
+    STA VBLANK
+    LDA #$FF
+    STA GRP0
+    LDA #$86
+    STA COLUP0
+    LDX #200
+L1: STA WSYNC
+    DEX
+    BNE L1
+    STA WSYNC
+    LDA #2
+""" + "    NOP\n" * 20 + """    STA RESP0
+    STA VSYNC
+    STA WSYNC
+    STA WSYNC
+    LDA #0
+    STA VSYNC
+    LDX #58
+L2: STA WSYNC
+    DEX
+    BNE L2
+    JMP Frame
+""" + _VECTORS

@@ -470,16 +470,27 @@ def _delay_programs():
         row0 = "    NOP\n" * k + "    LDA #$FF\n    STA $0E\n" + "    NOP\n" * 2 + "    LDA #$00\n    STA $1B\n"
         out.append(micro.static_frame(pokes=[(0x09, 0x1E), (0x08, 0x44), (0x06, 0x86), (0x1B, 0xFF), (0x0E, 0x00)],
                                       positions=[(0x10, 16)], kernel_row0=row0, store_collisions=True))
+    # mid-line RESP0 / RESM1 (RESxx start delay, R#36) with copies, a missile and a playfield to
+    # collide with; the reset at the end of row 0 leaves the delay pending into the frame's end
+    for k, nusiz in ((10, 3), (14, 0x16), (30, 1)):
+        row0 = ("    NOP\n" * k + "    STA $10\n    STA $13\n")
+        out.append(micro.static_frame(pokes=[(0x09, 0x1E), (0x06, 0x86), (0x07, 0xC8), (0x1B, 0xFF), (0x04, nusiz),
+                                             (0x05, nusiz), (0x1E, 2), (0x0D, 0xF0)],
+                                      positions=[(0x10, 10), (0x13, 12)], kernel_row0=row0, store_collisions=True))
+    # a frame that ends (VSYNC) on the line of a visible RESP0: the start delay is pending at the
+    # frame boundary (snapshot byte 63) and shows on the next frame's line 0 (window at ystart 0)
+    out.append(micro.m23_resp_at_vsync())
     return out
 
 
-@pytest.mark.parametrize("case", range(3))
+@pytest.mark.parametrize("case", range(7))
 def test_tia_delays_static_frames_raw(case):
-    """Static frames with mid-line playfield and GRP writes, RAW frames every step, with the
-    delayed register effects on: frames, collision latches and state equal the oracle's."""
+    """Static frames with mid-line playfield, GRP and RESxx writes, RAW frames every step, with
+    the delayed register effects on (R#35, R#36): frames, collision latches and the state
+    (byte 63 included) equal the oracle's."""
     rom = micro.build(_delay_programs()[case])
     gpu, ref = pair([rom], 8, 1, "raw", reset_cache_size=2, startup_frames=4, max_random_frames=3,
-                    tia_delays=1)
+                    tia_delays=1, ystart=0 if case == 6 else 34)
     run_parity(gpu, ref, 6)
 
 

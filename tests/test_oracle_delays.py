@@ -87,3 +87,64 @@ def test_delays_off_by_default_is_the_r4_model(orc):
         _, fa, _, _ = orc.run_frame(rom, a)
         _, fb, _, _ = orc.run_frame(rom, b, tia_delays=0)
         assert (fa == fb).all() and (a == b).all()
+
+
+# ---- RESxx start delay [R#36] ----------------------------------------------------------------
+def row0_resp_hp(k):
+    """`STA RESP0` after k NOPs on window row 0 ends at cycle 9 + 2k + 3: colour clock 36 + 6k,
+    hp = 6k - 32 (visible for k >= 6); the player lands at hp + 5 [R#10]."""
+    return 6 * k - 32
+
+
+@pytest.mark.parametrize("nusiz,copies", [(0, [0]), (1, [0, 16]), (3, [0, 16, 32])])
+@pytest.mark.parametrize("k", [10, 14])
+def test_resp_start_delay(orc, nusiz, copies, k):
+    # player 0 (GRP0 = $FF) first placed at p0 = 6 by a VBLANK RESP0 after 10 NOPs (hp = 1);
+    # row 0 strobes RESP0 again at visible hp = 6k - 32: the player moves to p1 = hp + 5
+    p0, hp = 6, row0_resp_hp(k)
+    p1 = hp + 5
+    row0 = "    NOP\n" * k + "    STA $10\n"
+    src = micro.static_frame(pokes=[(COLUBK, BK), (COLUP0, C0), (GRP0, 0xFF), (0x04, nusiz)],
+                             positions=[(RESP0, 10)], kernel_row0=row0)
+    for delays in (0, 1):
+        fb = run(orc, src, delays)
+        want0 = np.full(160, BK >> 1, np.uint8)
+        for c in copies:                # before the strobe: the copies at the old position
+            a, b = p0 + c, p0 + c + 8
+            want0[a:min(b, hp)] = C0 >> 1
+        for i, c in enumerate(copies):  # after it: the copies at the new position, except the
+            if delays and i == 0:       # first one on this line when the start delay is on
+                continue
+            a = max(p1 + c, hp)
+            want0[a:p1 + c + 8] = C0 >> 1
+        assert (fb[0] == want0).all(), (delays, np.nonzero(fb[0] != want0)[0])
+        want = np.full(160, BK >> 1, np.uint8)  # rows 1..: every copy at the new position
+        for c in copies:
+            want[p1 + c:p1 + c + 8] = C0 >> 1
+        assert (fb[1:] == want[None, :]).all()
+
+
+def test_resp_in_hblank_has_no_start_delay(orc):
+    # a strobe in HBLANK (the VBLANK positioning line, hp < 0) draws on its own line
+    src = micro.static_frame(pokes=[(COLUBK, BK), (COLUP0, C0), (GRP0, 0xFF)], positions=[(RESP0, 3)])
+    for delays in (0, 1):
+        fb = run(orc, src, delays)
+        assert (fb == run(orc, src, 0)).all()
+
+
+def test_start_delay_pending_at_frame_boundary(orc):
+    # M23: player 0 reset to 72 at hp = 67, VSYNC written at pixel 76 of the same line; the new
+    # frame's line 0 continues that line: pixels 76..79 of the player, unless the start delay
+    # suppresses the first copy, which the snapshot then carries in byte 63 (bit 0 = P0)
+    rom = micro.build(micro.m23_resp_at_vsync())
+    for delays in (0, 1):
+        s = orc.power_on(rom)
+        for _ in range(3):
+            st, fb, _, _ = orc.run_frame(rom, s, ystart=0, tia_delays=delays)
+            assert st == 0
+        assert s[63] == delays
+        assert s[56] == 72                                    # posP0
+        row0 = np.zeros(160, np.uint8)
+        if not delays:
+            row0[76:80] = C0 >> 1
+        assert (fb[0] == row0).all(), (delays, np.nonzero(fb[0])[0])
