@@ -127,6 +127,8 @@ std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, 
   cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
   cule::jit::Translation t = tr.run(gray, simt, ws);
   if (!t.ok) { err = t.why; return {}; }
+  // ablation switch (measurement only): rebuild every coverage mask on every span
+  if (getenv("CULE_TIA_NO_MASK_CACHE")) t.source = "#define CULE_TIA_NO_MASK_CACHE 1\n" + t.source;
   *n_insn = t.n_insn;
   if (const char* dump = getenv("CULE_JIT_DUMP")) {
     if (FILE* f = fopen(dump, "w")) { fwrite(t.source.data(), 1, t.source.size(), f); fclose(f); }

@@ -151,6 +151,7 @@ struct Tia {
     posP0 = h & 0xFF; posP1 = (h >> 8) & 0xFF; posM0 = (h >> 16) & 0xFF; posM1 = h >> 24;
     posBL = k & 0xFF; coll = k >> 16;
     t_tia = w[8 * s];
+    mdirty = 0x3Fu;
   }
   __device__ __forceinline__ void store(uint32_t* w, uint32_t s) const {
     w[0] = colup0 | (colup1 << 8) | (colupf << 16) | (colubk << 24);
@@ -183,6 +184,10 @@ struct Tia {
     }
   };
   struct Masks { W5 p0, p1, m0, m1, bl, pf; };
+  // coverage masks kept across the spans of a replay, rebuilt only for the objects a write
+  // changed (mdirty bits 0 P0, 1 P1, 2 M0, 3 M1, 4 BL, 5 PF; all set at load)
+  Masks mc;
+  uint32_t mdirty;
 
   // NUSIZ copy set: bit0 +0, bit1 +16, bit2 +32, bit3 +64
   __device__ __forceinline__ static uint32_t copies(uint32_t mode) { return (0x1D197531u >> (4 * mode)) & 0xF; }
@@ -211,6 +216,30 @@ struct Tia {
     const uint32_t mode = nusiz & 7;
     const uint32_t pat = (1u << (1u << ((nusiz >> 4) & 3))) - 1u;
     place_copies(m, pat, pos, ((mode == 5 || mode == 7) ? 1u : copies(mode)) & ~skip_first);
+  }
+  __device__ __forceinline__ void refresh_masks() {
+#ifdef CULE_TIA_NO_MASK_CACHE
+    mdirty = 0x3Fu;
+#endif
+    if (mdirty & 1u) player_mask(mc.p0, posP0, nusiz0, f(7) ? grp0o : grp0n, f(1), rdel & 1u);
+    if (mdirty & 2u) player_mask(mc.p1, posP1, nusiz1, f(8) ? grp1o : grp1n, f(2), (rdel >> 1) & 1u);
+    if (mdirty & 4u) missile_mask(mc.m0, posM0, nusiz0, f(3) && !f(10), (rdel >> 2) & 1u);
+    if (mdirty & 8u) missile_mask(mc.m1, posM1, nusiz1, f(4) && !f(11), (rdel >> 3) & 1u);
+    if (mdirty & 16u) {
+      mc.bl.zero();
+      if (f(9) ? f(6) : f(5)) mc.bl.place((1u << (1u << ((ctrlpf >> 4) & 3))) - 1u, posBL);
+    }
+    if (mdirty & 32u) {
+      const uint32_t left = ((pf0 >> 4) & 0xF) | (rev8(pf1) << 4) | ((pf2 & 0xFF) << 12);
+      const uint32_t right = (ctrlpf & 1) ? (__brev(left) >> 12) : left;
+      const uint64_t cells = (uint64_t)left | ((uint64_t)right << 20);
+      mc.pf.a = spread4((uint32_t)cells);
+      mc.pf.b = spread4((uint32_t)(cells >> 8));
+      mc.pf.c = spread4((uint32_t)(cells >> 16));
+      mc.pf.d = spread4((uint32_t)(cells >> 24));
+      mc.pf.e = spread4((uint32_t)(cells >> 32));
+    }
+    mdirty = 0u;
   }
   __device__ __forceinline__ void build_masks(Masks& M) const {
     player_mask(M.p0, posP0, nusiz0, f(7) ? grp0o : grp0n, f(1), rdel & 1u);
@@ -370,13 +399,16 @@ struct Tia {
     const uint32_t h0 = t0 - l0 * 228u, h1 = t_to - l1 * 228u;
     const uint32_t xa0 = h0 > 68u ? h0 - 68u : 0u;
     const uint32_t xb1 = h1 > 68u ? h1 - 68u : 0u;
+    // a span inside one line with no visible clock (the writes right after a WSYNC, in HBLANK)
+    // neither draws nor collides
+    if (l1 == l0 && xb1 <= xa0) return;
     const bool vblank = f(0) != 0u;
     const bool need_coll = !vblank && open_pairs() != 0u;
     const uint32_t w0 = ystart, w1 = ystart + (uint32_t)kFrameH;  // window lines [w0, w1)
     const bool any_win = render && l1 >= w0 && l0 < w1;
     if (!need_coll && !any_win) return;
-    Masks M;
-    if (!vblank) build_masks(M);
+    if (!vblank && mdirty) refresh_masks();
+    const Masks& M = mc;
     if (need_coll) {
       // collisions depend on x only: the union of the span's visible x ranges suffices
       if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) {
@@ -404,38 +436,39 @@ struct Tia {
     int32_t hp = (int32_t)h - 68;
     switch (r) {
       case 0x01: setf(0, (v >> 1) & 1); break;
-      case 0x04: nusiz0 = v; break;
-      case 0x05: nusiz1 = v; break;
+      case 0x04: nusiz0 = v; mdirty |= 1u | 4u; break;
+      case 0x05: nusiz1 = v; mdirty |= 2u | 8u; break;
       case 0x06: colup0 = v; break;
       case 0x07: colup1 = v; break;
       case 0x08: colupf = v; break;
       case 0x09: colubk = v; break;
-      case 0x0A: ctrlpf = v; break;
-      case 0x0B: setf(1, v >> 3); break;
-      case 0x0C: setf(2, v >> 3); break;
-      case 0x0D: pf0 = v; break;
-      case 0x0E: pf1 = v; break;
-      case 0x0F: pf2 = v; break;
+      case 0x0A: ctrlpf = v; mdirty |= 16u | 32u; break;
+      case 0x0B: setf(1, v >> 3); mdirty |= 1u; break;
+      case 0x0C: setf(2, v >> 3); mdirty |= 2u; break;
+      case 0x0D: pf0 = v; mdirty |= 32u; break;
+      case 0x0E: pf1 = v; mdirty |= 32u; break;
+      case 0x0F: pf2 = v; mdirty |= 32u; break;
       case 0x10: case 0x11: case 0x12: case 0x13: case 0x14: {
         uint32_t base = r <= 0x11 ? 5u : 4u;
         uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
         if (r == 0x10) posP0 = p; else if (r == 0x11) posP1 = p;
         else if (r == 0x12) posM0 = p; else if (r == 0x13) posM1 = p; else posBL = p;
         if (delays && hp >= 0 && r != 0x14) rdel |= 1u << (r - 0x10);  // RESxx start delay (R#36)
+        mdirty |= 1u << (r - 0x10);  // (bits 0 P0 .. 4 BL follow the register order)
       } break;
-      case 0x1B: grp0n = v; grp1o = grp1n; break;
-      case 0x1C: grp1n = v; grp0o = grp0n; setf(6, f(5)); break;
-      case 0x1D: setf(3, v >> 1); break;
-      case 0x1E: setf(4, v >> 1); break;
-      case 0x1F: setf(5, v >> 1); break;
+      case 0x1B: grp0n = v; grp1o = grp1n; mdirty |= 1u | 2u; break;
+      case 0x1C: grp1n = v; grp0o = grp0n; setf(6, f(5)); mdirty |= 1u | 2u | 16u; break;
+      case 0x1D: setf(3, v >> 1); mdirty |= 4u; break;
+      case 0x1E: setf(4, v >> 1); mdirty |= 8u; break;
+      case 0x1F: setf(5, v >> 1); mdirty |= 16u; break;
       case 0x20: hmp0 = v >> 4; break;
       case 0x21: hmp1 = v >> 4; break;
       case 0x22: hmm0 = v >> 4; break;
       case 0x23: hmm1 = v >> 4; break;
       case 0x24: hmbl = v >> 4; break;
-      case 0x25: setf(7, v); break;
-      case 0x26: setf(8, v); break;
-      case 0x27: setf(9, v); break;
+      case 0x25: setf(7, v); mdirty |= 1u; break;
+      case 0x26: setf(8, v); mdirty |= 2u; break;
+      case 0x27: setf(9, v); mdirty |= 16u; break;
       case 0x28: case 0x29: {
         const int b = r == 0x28 ? 10 : 11;
         uint32_t nv = (v >> 1) & 1;
@@ -445,6 +478,7 @@ struct Tia {
           if (r == 0x28) posM0 = (posP0 + c) % 160u; else posM1 = (posP1 + c) % 160u;
         }
         setf(b, nv);
+        mdirty |= r == 0x28 ? 4u : 8u;
       } break;
       case 0x2A: {
         auto mv = [](uint32_t p, uint32_t hm) -> uint32_t {
@@ -454,6 +488,7 @@ struct Tia {
         posP0 = mv(posP0, hmp0); posP1 = mv(posP1, hmp1); posM0 = mv(posM0, hmm0);
         posM1 = mv(posM1, hmm1); posBL = mv(posBL, hmbl);
         if (h < 68u) comb_line = (int32_t)line;
+        mdirty |= 31u;
       } break;
       case 0x2B: hmp0 = hmp1 = hmm0 = hmm1 = hmbl = 0; break;
       case 0x2C: coll = 0; break;
@@ -500,7 +535,7 @@ __device__ __forceinline__ void flush_lane(uint32_t* tw, uint32_t* pw_w, const u
       if (to >= le) { to = le; line_end = true; }
     }
     t.catch_up(to, render, pw, ystart, gray);
-    if (line_end) { t.rdel = 0u; continue; }
+    if (line_end) { t.mdirty |= t.rdel; t.rdel = 0u; continue; }
     if (k == n) break;
     t.apply(r, e & 0xFFu, T, delays);
     ++k;
