@@ -122,13 +122,15 @@ RomSet make_romset(const uint8_t* const* roms, const size_t* rom_lens, int n_rom
 }
 
 // translate + compile (or fetch from the caches) the JIT step kernel for a ROM set
-std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, bool ws, size_t* n_insn,
+std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, bool ws, bool delays, size_t* n_insn,
                             double* secs, bool* from_disk, std::string& err) {
   cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
   cule::jit::Translation t = tr.run(gray, simt, ws);
   if (!t.ok) { err = t.why; return {}; }
   // ablation switch (measurement only): rebuild every coverage mask on every span
   if (getenv("CULE_TIA_NO_MASK_CACHE")) t.source = "#define CULE_TIA_NO_MASK_CACHE 1\n" + t.source;
+  // the kernel is compiled for one setting of the delayed register effects (tia.cuh CULE_DELAYS_ON)
+  t.source = std::string("#define CULE_TIA_DELAYS ") + (delays ? "1" : "0") + "\n" + t.source;
   *n_insn = t.n_insn;
   if (const char* dump = getenv("CULE_JIT_DUMP")) {
     if (FILE* f = fopen(dump, "w")) { fwrite(t.source.data(), 1, t.source.size(), f); fclose(f); }
@@ -512,7 +514,7 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
     else {
       RomSet rs = make_romset(roms, rom_lens, n_roms);
-      cubin = jit_cubin(rs, n_roms, g, true, ws, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+      cubin = jit_cubin(rs, n_roms, g, true, ws, cfg->tia_delays != 0, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
     }
     // envs per warp (CULE_VEPW overrides: power of two <= 32; measured: 32 from 32768 envs, 16
     // from 8192, else 8) and warps per block: as many warps as the envs need to cover every SM,
@@ -572,7 +574,8 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
     else {
       RomSet rs = make_romset(roms, rom_lens, n_roms);
-      cubin = jit_cubin(rs, n_roms, g, false, false, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
+      cubin = jit_cubin(rs, n_roms, g, false, false, cfg->tia_delays != 0, &e->jit_insn, &e->jit_compile_s, &from_disk,
+                        jerr);
     }
     CUresult cr = CUDA_SUCCESS;
     if (!cubin.empty()) {
@@ -736,6 +739,7 @@ static int validate_snapshot(const cule_env* e, const uint8_t* s, size_t i) {
   if (fc >= 76u * (uint32_t)e->cfg.line_cap) return fail(CULE_E_INVAL, at + "fc beyond the line cap");
   if (s[62] > 2) return fail(CULE_E_INVAL, at + "fault code not in {0,1,2}");
   if (s[63] > 15) return fail(CULE_E_INVAL, at + "start-delay bits (byte 63) not in [0, 15]");
+  if (s[63] && !e->cfg.tia_delays) return fail(CULE_E_INVAL, at + "start-delay bits (byte 63) need tia_delays = 1");
   return CULE_OK;
 }
 
@@ -821,8 +825,8 @@ int cule_jit_prepare_engine(const uint8_t* const* roms, const size_t* rom_lens, 
   bool from_disk = false;
   std::string err;
   std::vector<char> cubin =
-      jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, engine != CULE_ENGINE_JIT, engine == CULE_ENGINE_WSVJIT, &n_insn,
-                &secs, &from_disk, err);
+      jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, engine != CULE_ENGINE_JIT, engine == CULE_ENGINE_WSVJIT, false,
+                &n_insn, &secs, &from_disk, err);
   if (cubin.empty()) return fail(CULE_E_CUDA, "JIT: " + err);
   if (info && info_len) {
     snprintf(info, info_len, "%zu instructions translated, cubin %zu bytes, %s %.1f s, cache %s", n_insn,

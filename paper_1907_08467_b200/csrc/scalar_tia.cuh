@@ -107,7 +107,7 @@ struct TiaP {
         if (r == 0x14u) w7 = with_byte(w7, 0, p);
         else w6 = with_byte(w6, (int)(r - 0x10u), p);
         // RESxx start delay (R#36): w4 byte 3, bits 0 P0 .. 3 M1, for the rest of this line
-        if (delays && hp >= 0 && r != 0x14u) w4 |= 1u << (24u + (r - 0x10u));
+        if (CULE_DELAYS_ON(delays) && hp >= 0 && r != 0x14u) w4 |= 1u << (24u + (r - 0x10u));
       } break;
       case 0x1B:  // GRP0; GRP1 old <- new
         w2 = with_byte(w2, 2, v); w3 = with_byte(w3, 1, byte_of(w3, 0));
@@ -454,7 +454,7 @@ __device__ __forceinline__ uint32_t flush_coop(uint32_t* tw, const uint32_t* lg,
     const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
     uint32_t to = k < n ? effect_clock(T, r, delays) : T;
     bool line_end = false;
-    if (t.w4 >> 24) {
+    if (CULE_DELAYS_ON(delays) && (t.w4 >> 24)) {
       const uint32_t le = (t.t / 228u + 1u) * 228u;
       if (to >= le) { to = le; line_end = true; }
     }

@@ -15,6 +15,16 @@
 #pragma once
 #include <stdint.h>
 
+// The delayed register effects (R#35, R#36) are a run-time option of the interpreter engines;
+// a translated kernel is compiled for one setting (CULE_TIA_DELAYS 0 or 1), and with 0 every
+// delay test below folds away.  With the option off no start delay can exist (the reset cache
+// has none, cule_set_state rejects a nonzero byte 63).
+#if defined(CULE_TIA_DELAYS) && CULE_TIA_DELAYS == 0
+#define CULE_DELAYS_ON(d) false
+#else
+#define CULE_DELAYS_ON(d) ((d) != 0u)
+#endif
+
 namespace cule {
 
 constexpr int kFrameW = 160;
@@ -453,7 +463,7 @@ struct Tia {
         uint32_t p = hp < -2 ? base - 2u : (uint32_t)(hp + (int32_t)base) % 160u;
         if (r == 0x10) posP0 = p; else if (r == 0x11) posP1 = p;
         else if (r == 0x12) posM0 = p; else if (r == 0x13) posM1 = p; else posBL = p;
-        if (delays && hp >= 0 && r != 0x14) rdel |= 1u << (r - 0x10);  // RESxx start delay (R#36)
+        if (CULE_DELAYS_ON(delays) && hp >= 0 && r != 0x14) rdel |= 1u << (r - 0x10);  // RESxx start delay (R#36)
         mdirty |= 1u << (r - 0x10);  // (bits 0 P0 .. 4 BL follow the register order)
       } break;
       case 0x1B: grp0n = v; grp1o = grp1n; mdirty |= 1u | 2u; break;
@@ -502,7 +512,7 @@ struct Tia {
 // 4*ceil(x/4), GRP0/GRP1 one colour clock later; without delays, and for every other register,
 // T itself (R#4).  The replay catches the TIA up to the effect clock, then applies the write.
 __device__ __forceinline__ uint32_t effect_clock(uint32_t T, uint32_t r, uint32_t delays) {
-  if (!delays) return T;
+  if (!CULE_DELAYS_ON(delays)) return T;
   if (r - 0x0Du < 3u) {
     const uint32_t h = T % 228u;
     const uint32_t d = h > 68u ? (h - 68u) & 3u : 0u;
@@ -530,7 +540,7 @@ __device__ __forceinline__ void flush_lane(uint32_t* tw, uint32_t* pw_w, const u
     const uint32_t T = e >> 14, r = (e >> 8) & 0x3Fu;
     uint32_t to = k < n ? effect_clock(T, r, delays) : t_final;
     bool line_end = false;
-    if (t.rdel) {
+    if (CULE_DELAYS_ON(delays) && t.rdel) {
       const uint32_t le = (t.t_tia / 228u + 1u) * 228u;
       if (to >= le) { to = le; line_end = true; }
     }

@@ -304,8 +304,11 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t bar_s, uint32_t parity) {
   asm volatile("{\n .reg .pred p;\n WS_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WS_WAIT_%=;\n}\n"
                ::"r"(bar_s), "r"(parity) : "memory");
 }
+// the two warps of a pair (named barrier 1 + pair; the non-aligned form: the warps arrive from
+// different code)
 __device__ __forceinline__ void pair_sync(uint32_t pair) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1u + pair) : "memory");
+  __syncwarp();
+  asm volatile("barrier.sync %0, 64;" ::"r"(1u + pair) : "memory");
 }
 
 // CPU half of a frame end (R#6, R#24): clocks rebased to the VSYNC line, canonical timer stamp;
