@@ -202,7 +202,7 @@ struct Tia {
   // NUSIZ copy set: bit0 +0, bit1 +16, bit2 +32, bit3 +64
   __device__ __forceinline__ static uint32_t copies(uint32_t mode) { return (0x1D197531u >> (4 * mode)) & 0xF; }
   __device__ __forceinline__ static void place_copies(W5& m, uint32_t pat, uint32_t pos, uint32_t cp) {
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < 4; ++c)
       if (cp & (1u << c)) {
         const uint32_t p = pos + (c == 0 ? 0u : (8u << c));
@@ -269,26 +269,30 @@ struct Tia {
     M.pf.e = spread4((uint32_t)(cells >> 32));
   }
 
-  // OR the collision latches of visible pixels [xa, xb) (bit 2r = d7, 2r+1 = d6 of register r)
-  __device__ __forceinline__ void collide(const Masks& M, uint32_t xa, uint32_t xb) {
-    uint32_t a00 = 0, a01 = 0, a02 = 0, a03 = 0, a04 = 0, a05 = 0, a06 = 0, a07 = 0, a08 = 0, a09 = 0,
-             a10 = 0, a11 = 0, a12 = 0, a14 = 0, a15 = 0;
-#pragma unroll
+  // bits of 32-pixel word [lo, lo+32) inside [xa, xb)
+  __device__ __forceinline__ static uint32_t range_word(uint32_t lo, uint32_t xa, uint32_t xb) {
+    const uint32_t s = xa > lo ? min(xa - lo, 32u) : 0u, e = xb > lo ? min(xb - lo, 32u) : 0u;
+    return e > s ? ((e - s == 32u ? 0xFFFFFFFFu : ((1u << (e - s)) - 1u)) << s) : 0u;
+  }
+  // OR the collision latches of the visible pixels [a0, b0) U [a1, b1) (bit 2r = d7, 2r+1 = d6 of
+  // register r).  A rolled loop over the five 32-pixel words (one copy of the body: the
+  // instruction cache, not the ALU, is what the replay runs short of), words outside the
+  // ranges skipped.
+  __device__ __forceinline__ void collide(const Masks& M, uint32_t a0, uint32_t b0, uint32_t a1, uint32_t b1) {
+    uint32_t acc = 0u;
+#pragma unroll 1
     for (int k = 0; k < 5; ++k) {
-      uint32_t lo = 32u * k;
-      uint32_t s = xa > lo ? min(xa - lo, 32u) : 0u, e = xb > lo ? min(xb - lo, 32u) : 0u;
-      uint32_t r = e > s ? ((e - s == 32u ? 0xFFFFFFFFu : ((1u << (e - s)) - 1u)) << s) : 0u;
-      uint32_t p0 = M.p0[k] & r, p1 = M.p1[k] & r, m0 = M.m0[k] & r, m1 = M.m1[k] & r,
-               bl = M.bl[k] & r, pf = M.pf[k] & r;
-      a00 |= m0 & p1; a01 |= m0 & p0; a02 |= m1 & p0; a03 |= m1 & p1;
-      a04 |= p0 & pf; a05 |= p0 & bl; a06 |= p1 & pf; a07 |= p1 & bl;
-      a08 |= m0 & pf; a09 |= m0 & bl; a10 |= m1 & pf; a11 |= m1 & bl;
-      a12 |= bl & pf; a14 |= p0 & p1; a15 |= m0 & m1;
+      const uint32_t r = range_word(32u * k, a0, b0) | range_word(32u * k, a1, b1);
+      if (!r) continue;
+      const uint32_t p0 = M.p0[k] & r, p1 = M.p1[k] & r, m0 = M.m0[k] & r, m1 = M.m1[k] & r,
+                     bl = M.bl[k] & r, pf = M.pf[k] & r;
+      acc |= ((m0 & p1) ? 1u : 0u) | ((m0 & p0) ? 2u : 0u) | ((m1 & p0) ? 4u : 0u) | ((m1 & p1) ? 8u : 0u) |
+             ((p0 & pf) ? 0x10u : 0u) | ((p0 & bl) ? 0x20u : 0u) | ((p1 & pf) ? 0x40u : 0u) |
+             ((p1 & bl) ? 0x80u : 0u) | ((m0 & pf) ? 0x100u : 0u) | ((m0 & bl) ? 0x200u : 0u) |
+             ((m1 & pf) ? 0x400u : 0u) | ((m1 & bl) ? 0x800u : 0u) | ((bl & pf) ? 0x1000u : 0u) |
+             ((p0 & p1) ? 0x4000u : 0u) | ((m0 & m1) ? 0x8000u : 0u);
     }
-    coll |= (a00 ? 1u : 0u) | (a01 ? 2u : 0u) | (a02 ? 4u : 0u) | (a03 ? 8u : 0u) |
-            (a04 ? 0x10u : 0u) | (a05 ? 0x20u : 0u) | (a06 ? 0x40u : 0u) | (a07 ? 0x80u : 0u) |
-            (a08 ? 0x100u : 0u) | (a09 ? 0x200u : 0u) | (a10 ? 0x400u : 0u) | (a11 ? 0x800u : 0u) |
-            (a12 ? 0x1000u : 0u) | (a14 ? 0x4000u : 0u) | (a15 ? 0x8000u : 0u);
+    coll |= acc;
   }
 
   __device__ __forceinline__ static uint32_t shade(uint32_t colu, const uint8_t* gray) {
@@ -324,11 +328,10 @@ struct Tia {
     return (x | (x << 3)) & 0x11111111u;
   }
 
-  // Pixels [xa, xb) of window row `row`.  Per 32-pixel coverage word the priority (R#13) is
-  // resolved on whole words into a 3-bit colour index per pixel (0 background, 1 playfield,
-  // 2 P0/M0, 3 P1/M1, 4 ball); per 16-pixel chunk the index bits become byte-permute selectors
-  // and four PRMTs pick the colour bytes.  Words outside the span are skipped (unrolled: every
-  // mask word is read with a constant index).
+  // Pixels [xa, xb) of window row `row`.  Per 16-pixel chunk the priority (R#13) is resolved
+  // on the chunk's coverage bits into a 3-bit colour index per pixel (0 background, 1 playfield,
+  // 2 P0/M0, 3 P1/M1, 4 ball); the index bits become byte-permute selectors and four PRMTs pick
+  // the colour bytes.
   __device__ __forceinline__ void render_span(const Masks& M, PixWriter& pw, uint32_t line, uint32_t row,
                                               uint32_t xa, uint32_t xb, const uint8_t* gray) {
     const uint32_t gbk = shade1(colubk, gray), g0 = shade1(colup0, gray), g1 = shade1(colup1, gray),
@@ -339,11 +342,13 @@ struct Tia {
     const uint32_t hiw = (g0 << 16) | (g1 << 24);
     const uint32_t Xl = gbk | ((score ? g0 : gbl) << 8) | hiw, Xr = gbk | ((score ? g1 : gbl) << 8) | hiw;
     const bool comb = (int32_t)line == comb_line;
-    const uint32_t c_lo = xa >> 4, c_hi = (xb - 1) >> 4;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      if (2u * k + 1u < c_lo || 2u * k > c_hi) continue;
-      const uint32_t a = M.p0[k] | M.m0[k], b = M.p1[k] | M.m1[k], l = M.bl[k], f = M.pf[k];
+    // one chunk per iteration, rolled (code size: see collide)
+#pragma unroll 1
+    for (uint32_t c = xa >> 4; c <= (xb - 1) >> 4; ++c) {
+      const int k = (int)(c >> 1);
+      const uint32_t sh = 16u * (c & 1u);
+      const uint32_t a = ((M.p0[k] | M.m0[k]) >> sh) & 0xFFFFu, b = ((M.p1[k] | M.m1[k]) >> sh) & 0xFFFFu,
+                     l = (M.bl[k] >> sh) & 0xFFFFu, f = (M.pf[k] >> sh) & 0xFFFFu;
       uint32_t e0, e1, eb, ep;
       if (!pfp) {
         e0 = a; e1 = b & ~a; eb = l & ~(a | b); ep = f & ~(a | b | l);
@@ -351,31 +356,27 @@ struct Tia {
         eb = l; ep = f & ~l; e0 = a & ~(l | f); e1 = b & ~(l | f | a);
       }
       const uint32_t i0 = ep | e1, i1 = e0 | e1, i2 = eb;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t c = 2u * k + h;
-        if (c < c_lo || c > c_hi) continue;
-        const uint32_t x0 = 16u * c, sh = 16u * h;
-        const uint32_t X = x0 < 80u ? Xl : Xr;
-        uint32_t sa = sel_bits(i0 >> sh), sb = sel_bits(i0 >> (sh + 8u));
-        if (((i1 | i2) >> sh) & 0xFFFFu) {  // (playfield-only chunks need one index bit)
-          sa |= (sel_bits(i1 >> sh) << 1) | (sel_bits(i2 >> sh) << 2);
-          sb |= (sel_bits(i1 >> (sh + 8u)) << 1) | (sel_bits(i2 >> (sh + 8u)) << 2);
-        }
-        uint32_t p0 = __byte_perm(X, gbl, sa), p1 = __byte_perm(X, gbl, sa >> 16);
-        const uint32_t p2 = __byte_perm(X, gbl, sb), p3 = __byte_perm(X, gbl, sb >> 16);
-        if (comb && c == 0) { p0 = pw.fill; p1 = pw.fill; }  // HMOVE comb, x < 8 (R#11)
-        if (xa <= x0 && xb >= x0 + 16u) {
-          pw.emit_full((int32_t)(row * 10u + c), p0, p1, p2, p3);
-        } else {
-          const uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 16u ? xb - x0 : 16u;
-          const uint32_t r = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-          pw.emit((int32_t)(row * 10u + c), p0, p1, p2, p3, nib_bytes(r), nib_bytes(r >> 4), nib_bytes(r >> 8),
-                  nib_bytes(r >> 12));
-        }
+      uint32_t sa = sel_bits(i0), sb = sel_bits(i0 >> 8u);
+      if (i1 | i2) {  // (playfield-only chunks need one index bit)
+        sa |= (sel_bits(i1) << 1) | (sel_bits(i2) << 2);
+        sb |= (sel_bits(i1 >> 8u) << 1) | (sel_bits(i2 >> 8u) << 2);
+      }
+      const uint32_t x0 = 16u * c;
+      const uint32_t X = x0 < 80u ? Xl : Xr;
+      uint32_t p0 = __byte_perm(X, gbl, sa), p1 = __byte_perm(X, gbl, sa >> 16);
+      const uint32_t p2 = __byte_perm(X, gbl, sb), p3 = __byte_perm(X, gbl, sb >> 16);
+      if (comb && c == 0) { p0 = pw.fill; p1 = pw.fill; }  // HMOVE comb, x < 8 (R#11)
+      if (xa <= x0 && xb >= x0 + 16u) {
+        pw.emit_full((int32_t)(row * 10u + c), p0, p1, p2, p3);
+      } else {
+        const uint32_t lo = xa > x0 ? xa - x0 : 0u, hi = xb < x0 + 16u ? xb - x0 : 16u;
+        const uint32_t r = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+        pw.emit((int32_t)(row * 10u + c), p0, p1, p2, p3, nib_bytes(r), nib_bytes(r >> 4), nib_bytes(r >> 8),
+                nib_bytes(r >> 12));
       }
     }
   }
+
   __device__ __forceinline__ static void render_black(PixWriter& pw, uint32_t row, uint32_t xa, uint32_t xb) {
     for (uint32_t c = xa >> 4; c <= (xb - 1) >> 4; ++c) {
       const uint32_t x0 = 16u * c;
@@ -421,14 +422,10 @@ struct Tia {
     const Masks& M = mc;
     if (need_coll) {
       // collisions depend on x only: the union of the span's visible x ranges suffices
-      if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) {
-        collide(M, 0u, 160u);
-      } else if (l1 == l0) {
-        if (xb1 > xa0) collide(M, xa0, xb1);
-      } else {
-        if (xa0 < 160u) collide(M, xa0, 160u);
-        if (xb1 > 0u) collide(M, 0u, xb1);
-      }
+      uint32_t a0 = xa0, b0 = 160u, a1 = 0u, b1 = xb1;                           // two partial lines
+      if (l1 > l0 + 1u || (l1 == l0 + 1u && xa0 <= xb1)) { a0 = 0u; b1 = 0u; }  // every x
+      else if (l1 == l0) { b0 = xb1; b1 = 0u; }                                  // one line
+      collide(M, a0, b0, a1, b1);
     }
     if (!any_win) return;
     const uint32_t la = l0 > w0 ? l0 : w0, lb = l1 < w1 - 1u ? l1 : w1 - 1u;

@@ -81,17 +81,19 @@ static_assert(kA84Bytes <= 32u * 4u * kVLaneWords, "the epilogue ring fits in th
 __device__ __forceinline__ void warp_area84_staged(const uint8_t* fa, const uint8_t* fb, uint8_t* out, uint32_t lane,
                                                    uint32_t ring_s, uint32_t cols_s) {
   const uint32_t nq = fb ? 100u : 50u;  // 16-byte chunks per group: frame fs, then frame fs-1
+  // group g's copies (one call site in the loop below: the prologue runs it for groups 0-2)
   auto issue = [&](uint32_t g) {
     if (g < 42u) {
       const uint32_t slot = ring_s + (g & 3u) * kA84Slot;
+#pragma unroll 1
       for (uint32_t q = lane; q < nq; q += 32u)
         cp_async16(slot + 16u * q, (q < 50u ? fa : fb) + 800u * g + 16u * (q < 50u ? q : q - 50u));
     }
     cp_async_commit();  // (an empty group past the end keeps the wait count uniform)
   };
-  issue(0u);
-  issue(1u);
-  issue(2u);
+#pragma unroll 1
+  for (uint32_t g = 0; g < 3u; ++g) issue(g);
+#pragma unroll 1
   for (uint32_t g = 0; g < 42u; ++g) {
     cp_async_wait<2>();  // group g has landed (groups g+1, g+2 may be in flight)
     __syncwarp();

@@ -17,6 +17,6 @@ timeout 900 python bench.py --config $c --no-cpu-baseline --sweep 0 --e4 0 --no-
 python -c "import json; d=json.loads(open('gpurun_out/b_$c.json').read().strip().splitlines()[-1]); print('$c', round(d['value']), d['ms_per_step'], d['config']['engine'], round(d['e2e']['value']))"
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/launch_bench.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:cule_v?jit -s 60 -c 1 -o gpurun_out/prof_cfg2 python bench.py --steps 3 --warmup 60 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/ncu_full.log 2>&1; echo "ncu cfg2 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:cule_v?jit -s 30 -c 1 -o gpurun_out/prof_cfg3 python bench.py --config cfg3 --steps 3 --warmup 30 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/ncu_cfg3.log 2>&1; echo "ncu cfg3 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:cule_v?jit -s 30 -c 1 -o gpurun_out/prof_cfg4 python bench.py --config cfg4 --steps 3 --warmup 30 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/ncu_cfg4.log 2>&1; echo "ncu cfg4 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cule_v?jit -s 250 -c 1 -o gpurun_out/prof_cfg2 python bench.py --steps 3 --warmup 250 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/ncu_full.log 2>&1; echo "ncu cfg2 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cule_v?jit -s 250 -c 1 -o gpurun_out/prof_cfg3 python bench.py --config cfg3 --steps 3 --warmup 250 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/ncu_cfg3.log 2>&1; echo "ncu cfg3 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cule_v?jit -s 250 -c 1 -o gpurun_out/prof_cfg4 python bench.py --config cfg4 --steps 3 --warmup 250 --no-cpu-baseline --no-variant --e2e-steps 1 --inference-steps 0 --vtrace 0 --sweep 0 --e4 0 > gpurun_out/ncu_cfg4.log 2>&1; echo "ncu cfg4 rc=$?"
