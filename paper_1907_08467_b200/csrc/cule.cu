@@ -123,7 +123,7 @@ RomSet make_romset(const uint8_t* const* roms, const size_t* rom_lens, int n_rom
 
 // translate + compile (or fetch from the caches) the JIT step kernel for a ROM set
 std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, bool ws, bool delays, size_t* n_insn,
-                            double* secs, bool* from_disk, std::string& err) {
+                            double* secs, bool* from_disk, std::string& err, uint32_t vlogcap = 32) {
   cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
   cule::jit::Translation t = tr.run(gray, simt, ws);
   if (!t.ok) { err = t.why; return {}; }
@@ -131,6 +131,7 @@ std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, 
   if (getenv("CULE_TIA_NO_MASK_CACHE")) t.source = "#define CULE_TIA_NO_MASK_CACHE 1\n" + t.source;
   // the kernel is compiled for one setting of the delayed register effects (tia.cuh CULE_DELAYS_ON)
   t.source = std::string("#define CULE_TIA_DELAYS ") + (delays ? "1" : "0") + "\n" + t.source;
+  if (simt && !ws && vlogcap != 32) t.source = "#define CULE_VLOGCAP " + std::to_string(vlogcap) + "\n" + t.source;
   *n_insn = t.n_insn;
   if (const char* dump = getenv("CULE_JIT_DUMP")) {
     if (FILE* f = fopen(dump, "w")) { fwrite(t.source.data(), 1, t.source.size(), f); fclose(f); }
@@ -496,13 +497,11 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
   // profiles/r02_engine_sweep.txt: one ROM at every env count; mixed ROM sets up to 16384 envs —
   // beyond that the batched engine amortises its datapath over 32 envs per warp and the
   // translated code of several ROMs crowds the instruction cache) and applies (idle skip off)
-  // translated engines (measured sweep, profiles/r02_vjit_sweep.txt): VJIT (one env per lane)
-  // once there are enough envs to fill warps of 16-32 lanes on every SM — 16384+ envs, or 8192+
-  // when several ROMs make the one-env-per-warp engine's replay the larger cost — else JIT
-  // (one env per warp) for one ROM at any count and mixed sets up to 16384 envs; neither has the
-  // idle-loop skip
+  // translated engines (measured sweep, profiles/r02_engine_sweep.txt): VJIT (one env per lane)
+  // from 8192 envs, or 4096 when several ROMs make the one-env-per-warp engine's replay the
+  // larger cost; else JIT (one env per warp); neither has the idle-loop skip
   const bool xlate = !cfg->idle_skip;
-  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && (num_envs >= 16384 || (n_roms > 1 && num_envs >= 8192));
+  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && (num_envs >= 8192 || (n_roms > 1 && num_envs >= 4096));
   bool jit_auto = want == CULE_ENGINE_AUTO && xlate && !vjit_auto && (n_roms == 1 || num_envs <= 16384);
   if (want == CULE_ENGINE_VJIT || want == CULE_ENGINE_WSVJIT || vjit_auto) {
     const bool ws = want == CULE_ENGINE_WSVJIT;
@@ -510,16 +509,10 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     auto& drv = cule::jit::driver();
     std::vector<char> cubin;
     bool from_disk = false;
-    if (!drv.ok) jerr = "CUDA driver entry points unavailable";
-    else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
-    else {
-      RomSet rs = make_romset(roms, rom_lens, n_roms);
-      cubin = jit_cubin(rs, n_roms, g, true, ws, cfg->tia_delays != 0, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr);
-    }
-    // envs per warp (CULE_VEPW overrides: power of two <= 32; measured: 32 from 32768 envs, 16
+    // envs per warp (CULE_VEPW overrides: power of two <= 32; measured: 32 from 16384 envs, 16
     // from 8192, else 8) and warps per block: as many warps as the envs need to cover every SM,
     // within the shared memory of one block per SM
-    uint32_t vepw = num_envs >= 32768 ? 32u : (num_envs >= 8192 ? 16u : 8u);
+    uint32_t vepw = num_envs >= 16384 ? 32u : (num_envs >= 8192 ? 16u : 8u);
     if (const char* v = getenv("CULE_VEPW")) {
       const int b = atoi(v);
       if (b >= 1 && b <= 32 && (b & (b - 1)) == 0) vepw = (uint32_t)b;
@@ -530,17 +523,27 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     if (optin <= 0) optin = 232448;
     // (warp-specialized: groups of envs per warp PAIR, which shares one set of lane areas)
     const uint32_t warps = ((uint32_t)num_envs + vepw - 1) / vepw;
-    const size_t lane_off = ws ? cule::wsvjit_lane_off(e->rom_bytes) : cule::vjit_lane_off(e->rom_bytes);
-    const uint32_t fit = (uint32_t)(((size_t)optin - lane_off) /
-                                    (32u * 4u * (ws ? cule::kWLaneWords : cule::kVLaneWords)));
     uint32_t wpb = (warps + (uint32_t)sm_count() - 1) / (uint32_t)sm_count();
     if (const char* v = getenv("CULE_VWPB")) wpb = (uint32_t)atoi(v);
+    // TIA log entries per lane (vjit_kernels.cuh CULE_VLOGCAP): 64 up to 8 warps per SM, else 32
+    uint32_t vcap = (!ws && wpb <= 8u) ? 64u : 32u;
+    if (const char* v = getenv("CULE_VLOGCAP")) vcap = (!ws && atoi(v) == 64) ? 64u : 32u;
+    const size_t lane_off = ws ? cule::wsvjit_lane_off(e->rom_bytes) : cule::vjit_lane_off(e->rom_bytes);
+    const uint32_t fit = (uint32_t)(((size_t)optin - lane_off) /
+                                    (32u * 4u * (ws ? cule::kWLaneWords : cule::vjit_lane_words(vcap))));
     wpb = std::max(1u, std::min({wpb, fit, (uint32_t)CULE_VWARPS / (ws ? 2u : 1u)}));
     e->vepw = vepw;
     e->vws = ws;
     e->vblock = (ws ? 64u : 32u) * wpb;
     e->vgrid = (warps + wpb - 1) / wpb;
-    e->vsmem = ws ? cule::wsvjit_smem_bytes(e->rom_bytes, wpb) : cule::vjit_smem_bytes(e->rom_bytes, e->vblock);
+    e->vsmem = ws ? cule::wsvjit_smem_bytes(e->rom_bytes, wpb) : cule::vjit_smem_bytes(e->rom_bytes, e->vblock, vcap);
+    if (!drv.ok) jerr = "CUDA driver entry points unavailable";
+    else if (cfg->idle_skip) jerr = "the translated engine has no idle-loop skip";
+    else {
+      RomSet rs = make_romset(roms, rom_lens, n_roms);
+      cubin = jit_cubin(rs, n_roms, g, true, ws, cfg->tia_delays != 0, &e->jit_insn, &e->jit_compile_s, &from_disk, jerr,
+                        vcap);
+    }
     CUresult cr = CUDA_SUCCESS;
     if (!cubin.empty()) {
       cr = drv.moduleLoadData(&e->jit_mod, cubin.data());
@@ -828,6 +831,13 @@ int cule_jit_prepare_engine(const uint8_t* const* roms, const size_t* rom_lens, 
       jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, engine != CULE_ENGINE_JIT, engine == CULE_ENGINE_WSVJIT, false,
                 &n_insn, &secs, &from_disk, err);
   if (cubin.empty()) return fail(CULE_E_CUDA, "JIT: " + err);
+  if (engine == CULE_ENGINE_VJIT) {  // both log capacities (cule_create picks by warps per SM)
+    double s2 = 0.0;
+    bool d2 = false;
+    if (jit_cubin(rs, n_roms, obs_mode == CULE_OBS_GRAY84, true, false, false, &n_insn, &s2, &d2, err, 64).empty())
+      return fail(CULE_E_CUDA, "JIT: " + err);
+    secs += s2;
+  }
   if (info && info_len) {
     snprintf(info, info_len, "%zu instructions translated, cubin %zu bytes, %s %.1f s, cache %s", n_insn,
              cubin.size(), from_disk ? "loaded from disk" : "compiled in", secs, cule::jit::cache_dir().c_str());

@@ -20,16 +20,24 @@ namespace cule {
 #ifndef CULE_VWARPS
 #define CULE_VWARPS 16  // most warps per block (launch bound); the host picks the block size
 #endif
-constexpr uint32_t kVLogCap = 32;
+// TIA log entries per lane: 64 while the warps of an SM fit one block (fewer flushes, and each
+// flush reloads the TIA and rebuilds its coverage masks), 32 when more warps per SM are needed;
+// the host compiles the kernel for one of them (CULE_VLOGCAP) and sizes shared memory to match
+#ifndef CULE_VLOGCAP
+#define CULE_VLOGCAP 32
+#endif
+constexpr uint32_t kVLogCap = CULE_VLOGCAP;
+constexpr uint32_t kWLogCap = 32;  // per buffer, warp-specialized variant
 constexpr uint32_t kVOffTw = 0, kVOffPw = 9, kVOffM = 18, kVOffRam = 50, kVOffLog = 82;
-constexpr uint32_t kVLaneWords = kVOffLog + kVLogCap + 1;
-static_assert(kVLaneWords % 2 == 1, "odd lane stride: conflict-free shared-memory fields");
+__host__ __device__ constexpr uint32_t vjit_lane_words(uint32_t cap) { return kVOffLog + cap + 1u; }
+constexpr uint32_t kVLaneWords = vjit_lane_words(kVLogCap);
+static_assert(kVLaneWords % 2 == 1 && vjit_lane_words(64u) % 2 == 1, "odd lane stride: conflict-free fields");
 static_assert(sizeof(SMach) == 4 * (kVOffRam - kVOffM), "SMach slot");
 
 // [mbarrier][area84 column weights][gray LUT][scalar decode table][ROM images][lanes]
 __host__ __device__ __forceinline__ size_t vjit_lane_off(uint32_t rom_bytes) { return scalar_rec_off(rom_bytes); }
-__host__ __device__ __forceinline__ size_t vjit_smem_bytes(uint32_t rom_bytes, uint32_t threads) {
-  return vjit_lane_off(rom_bytes) + (size_t)threads * kVLaneWords * 4u;
+__host__ __device__ __forceinline__ size_t vjit_smem_bytes(uint32_t rom_bytes, uint32_t threads, uint32_t cap) {
+  return vjit_lane_off(rom_bytes) + (size_t)threads * vjit_lane_words(cap) * 4u;
 }
 
 // ---- warp-specialized variant (NEXT-2): producer warps emulate, consumer warps render
@@ -76,12 +84,23 @@ template <int kN>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory"); }
 
 constexpr uint32_t kA84Slot = 1600u, kA84Bytes = 4u * kA84Slot;  // per-warp ring (shared memory)
-static_assert(kA84Bytes <= 32u * 4u * kVLaneWords, "the epilogue ring fits in the warp's lane areas");
+static_assert(kA84Bytes <= 32u * 4u * vjit_lane_words(32u), "the epilogue ring fits in the warp's lane areas");
 
 __device__ __forceinline__ void warp_area84_staged(const uint8_t* fa, const uint8_t* fb, uint8_t* out, uint32_t lane,
                                                    uint32_t ring_s, uint32_t cols_s) {
   const uint32_t nq = fb ? 100u : 50u;  // 16-byte chunks per group: frame fs, then frame fs-1
   // group g's copies (one call site in the loop below: the prologue runs it for groups 0-2)
+  // the lane's output columns (lane, lane + 32, lane + 64): first source column and the packed
+  // byte weights wc0 | wc1 << 8 | wc2 << 16, once per env
+  uint32_t cs[3], wpk[3];
+#pragma unroll
+  for (uint32_t u = 0; u < 3u; ++u) {
+    const uint32_t j = lane + 32u * u;
+    uint32_t cw = 0u;
+    if (j < 84u) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(cols_s + 4u * j) : "memory");
+    cs[u] = cw & 0xFFu;
+    wpk[u] = cw >> 8;
+  }
   auto issue = [&](uint32_t g) {
     if (g < 42u) {
       const uint32_t slot = ring_s + (g & 3u) * kA84Slot;
@@ -108,16 +127,22 @@ __device__ __forceinline__ void warp_area84_staged(const uint8_t* fa, const uint
       }
       __syncwarp();
     }
-    for (uint32_t j = lane; j < 84u; j += 32u) {
-      uint32_t cw;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(cols_s + 4u * j) : "memory");
-      const uint32_t c0 = cw & 0xFFu, wc0 = (cw >> 8) & 0xFFu, wc1 = (cw >> 16) & 0xFFu, wc2 = cw >> 24;
-      const uint32_t d2 = wc2 ? 2u : 0u;  // (weight 0: any in-row column)
+#pragma unroll
+    for (uint32_t u = 0; u < 3u; ++u) {  // output columns lane, lane + 32, lane + 64 (< 84)
+      const uint32_t j = lane + 32u * u;
+      if (j >= 84u) break;
+      // the five rows' weighted sums: bytes c0 .. c0+3 of each row by two aligned 32-bit loads
+      // and a funnel shift, weighted by one byte dot product (the 4th weight is 0; reading one
+      // byte past a row stays inside the ring slot)
+      const uint32_t q = slot + cs[u];
+      const uint32_t qa = q & ~3u, sh = 8u * (q & 3u);
       uint32_t h[5];
 #pragma unroll
       for (int r = 0; r < 5; ++r) {
-        const uint32_t q = slot + 160u * r + c0;
-        h[r] = wc0 * lds_u8(q) + wc1 * lds_u8(q + 1u) + wc2 * lds_u8(q + d2);
+        uint32_t lo, hi;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(qa + 160u * r) : "memory");
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(qa + 160u * r + 4u) : "memory");
+        h[r] = __dp4a(__funnelshift_r(lo, hi, sh), wpk[u], 0u);
       }
       const uint32_t S0 = 2u * h[0] + 2u * h[1] + h[2], S1 = h[2] + 2u * h[3] + 2u * h[4];
       uint32_t q0 = S0 / 200u, q1 = S1 / 200u;
@@ -394,7 +419,7 @@ __device__ __forceinline__ void wsvjit_kernel_body(const Params& p) {
       if (buf == 0u ? pending0 : pending1) wait_empty(buf);  // the consumer is done with this buffer
       M->log_len = 0u;
       const uint32_t ev = run_cpu_vjit(M, rom_all0, dtab0, ram0, smem_addr(lw + (buf ? kWOffL1 : kWOffL0)),
-                                       kVLogCap - 3u, cap_cycles, running);
+                                       kWLogCap - 3u, cap_cycles, running);
       bool need_sync = false;
       uint32_t tgt = 0u;
       if (running) {
