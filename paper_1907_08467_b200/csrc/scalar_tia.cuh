@@ -68,12 +68,16 @@ struct TiaP {
   __device__ __forceinline__ void setf(int b, uint32_t v) { w5 = (w5 & ~(1u << b)) | ((v & 1u) << b); }
   __device__ __forceinline__ uint32_t coll() const { return w7 >> 16; }
   __device__ __forceinline__ int32_t comb_line() const { return (int32_t)(int16_t)(w5 >> 16); }
+  // the presence bits travel in w7 byte 1 between replays (bit 15: valid; a state loaded from a
+  // snapshot has none and computes them once)
   __device__ __forceinline__ void load(const uint32_t* tw) {
     w0 = tw[0]; w1 = tw[1]; w2 = tw[2]; w3 = tw[3]; w4 = tw[4]; w5 = tw[5]; w6 = tw[6]; w7 = tw[7]; t = tw[8];
-    pres = p0_on() | (p1_on() << 1) | (m0_on() << 2) | (m1_on() << 3) | (ball_on() << 4) | (pf_on() << 5);
+    if (w7 & 0x8000u) pres = (w7 >> 8) & 0x3Fu;
+    else pres = p0_on() | (p1_on() << 1) | (m0_on() << 2) | (m1_on() << 3) | (ball_on() << 4) | (pf_on() << 5);
   }
   __device__ __forceinline__ void store(uint32_t* tw) const {
-    tw[0] = w0; tw[1] = w1; tw[2] = w2; tw[3] = w3; tw[4] = w4; tw[5] = w5; tw[6] = w6; tw[7] = w7; tw[8] = t;
+    tw[0] = w0; tw[1] = w1; tw[2] = w2; tw[3] = w3; tw[4] = w4; tw[5] = w5; tw[6] = w6;
+    tw[7] = (w7 & 0xFFFF00FFu) | 0x8000u | (pres << 8); tw[8] = t;
   }
   __device__ __forceinline__ uint32_t grp0() const { return byte_of(w2, f(7) ? 3 : 2); }
   __device__ __forceinline__ uint32_t grp1() const { return byte_of(w3, f(8) ? 1 : 0); }
