@@ -41,7 +41,7 @@ struct SMach {
   uint32_t pa_T, pa_coll;  // latches kept for a phase-A read at pa_T (see run_cpu)
   uint32_t abort_T, abort_pa;
   uint32_t idle_skip;  // exact idle-loop skip enabled (cule_config.idle_skip)
-  uint32_t pad1;
+  uint32_t shd;        // shared address of the TIA write shadow (R#37), 0 = no write elision
 };
 static_assert(sizeof(SMach) == 32 * 4, "SMach is 32 words");
 
@@ -49,6 +49,64 @@ static_assert(sizeof(SMach) == 32 * 4, "SMach is 32 words");
 // RSYNC, audio and the unused range never reach the log): 0x01, 0x04-0x14, 0x1B-0x2C
 constexpr uint64_t kTiaEffect = (1ull << 0x01) | (((1ull << 0x15) - 1) & ~((1ull << 0x04) - 1)) |
                                 (((1ull << 0x2D) - 1) & ~((1ull << 0x1B) - 1));
+
+// ---- TIA write elision (DESIGN.md §2 R#37) ---------------------------------------------------
+// A logged write whose register already holds the written value leaves the TIA state exactly as
+// it was, so the replay would only split a span of constant registers in two.  The producer keeps
+// a shadow of what the log has written this step and drops such writes.  Shadow entry shd_idx(r)
+// (u16; scalar_predecode.h) is the last raw byte logged for register r, or a token 0x100 + k
+// (unknown: unequal to every byte and to every other entry); entries kShdG0o / kShdG1o / kShdEbo
+// shadow the VDEL copies GRP0 old, GRP1 old and ENABL old.  Registers whose write is a pure store
+// of the value (kTiaPure): NUSIZ0 ... PF2 (0x04-0x0F) and ENAM0 ... RESMP1 (0x1D-0x29; a RESMP
+// write acts only on a change of D1).  GRP0 / GRP1 also copy the other player's (and the ball's)
+// new value into its old one, so they are dropped only when both are unchanged; HMCLR zeroes the
+// five motion registers; the strobes (RESxx, HMOVE, CXCLR) and VBLANK always reach the log.
+__device__ __forceinline__ uint32_t ld_shd(uint32_t shd, uint32_t k) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(shd + 2u * k) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shd(uint32_t shd, uint32_t k, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(shd + 2u * k), "r"(v) : "memory");
+}
+// every entry unknown: by the whole warp (one entry per lane) ...
+__device__ __forceinline__ void shd_init_warp(uint32_t shd, uint32_t lane) { st_shd(shd, lane, 0x100u + lane); }
+// ... or by one lane (its own shadow; 4-byte aligned)
+__device__ __forceinline__ void shd_init_lane(uint32_t shd) {
+#pragma unroll 1
+  for (uint32_t k = 0; k < kShdEntries; k += 2u)
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(shd + 2u * k), "r"((0x100u + k) | ((0x101u + k) << 16)) : "memory");
+}
+// the shadow after a write of byte v to TIA effect register r; false when the write changes
+// nothing (drop it), true when it must reach the log
+__device__ __forceinline__ bool shd_write(uint32_t shd, uint32_t r, uint32_t v) {
+  if ((kTiaPure >> r) & 1ull) {
+    if (ld_shd(shd, shd_idx(r)) == v) return false;
+    st_shd(shd, shd_idx(r), v);
+    return true;
+  }
+  constexpr uint32_t G0 = shd_idx(0x1Bu), G1 = shd_idx(0x1Cu), EB = shd_idx(0x1Fu);
+  if (r == 0x1Bu) {  // GRP0; GRP1 old <- GRP1 new
+    const uint32_t g1n = ld_shd(shd, G1);
+    if (ld_shd(shd, G0) == v && ld_shd(shd, kShdG1o) == g1n) return false;
+    st_shd(shd, G0, v);
+    st_shd(shd, kShdG1o, g1n);
+    return true;
+  }
+  if (r == 0x1Cu) {  // GRP1; GRP0 old <- GRP0 new; ENABL old <- ENABL new
+    const uint32_t g0n = ld_shd(shd, G0), ebn = ld_shd(shd, EB);
+    if (ld_shd(shd, G1) == v && ld_shd(shd, kShdG0o) == g0n && ld_shd(shd, kShdEbo) == ebn) return false;
+    st_shd(shd, G1, v);
+    st_shd(shd, kShdG0o, g0n);
+    st_shd(shd, kShdEbo, ebn);
+    return true;
+  }
+  if (r == 0x2Bu) {  // HMCLR: HMP0 ... HMBL read as written with 0
+#pragma unroll 1
+    for (uint32_t k = shd_idx(0x20u); k <= shd_idx(0x24u); ++k) st_shd(shd, k, 0u);
+  }
+  return true;
+}
 
 __device__ __forceinline__ uint32_t s_coll_bits(uint32_t coll, uint32_t r) {
   return (((coll >> (2 * r)) & 1u) << 7) | (((coll >> (2 * r + 1)) & 1u) << 6);
@@ -303,7 +361,7 @@ __device__ __noinline__ uint32_t s_gen_one(SMach* M, uint32_t rom_all0, uint32_t
           st_ram(ram0 + (a & 0x7Fu), val & 0xFFu);
         } else if (!(a & 0x1080u)) {  // TIA: effect registers go to the log (R#4)
           const uint32_t r = a & 0x3Fu;
-          if ((kTiaEffect >> r) & 1ull) {
+          if (((kTiaEffect >> r) & 1ull) && (!M->shd || shd_write(M->shd, r, val & 0xFFu))) {
             st_log(lg0 + 4u * log_len, ((3u * now) << 14) | (r << 8) | (val & 0xFFu));
             ++log_len;
           } else if (r == 0x02u) {

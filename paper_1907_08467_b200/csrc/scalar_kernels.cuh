@@ -19,11 +19,12 @@
 namespace cule {
 
 // per-warp shared memory: [RAM 128][TIA words 48][SMach 128][state staging 80][log 4*kSLogCap]
-// [fused-observation ring 3 x 160][shaded colours 16]
+// [fused-observation ring 3 x 160][shaded colours 16][TIA write shadow 64 x u16 (R#37)]
 constexpr uint32_t kSLogCap = 128;
 constexpr uint32_t kSOffTia = 128, kSOffMach = 176, kSOffStg = 304, kSOffLog = 384;
 constexpr uint32_t kSOffRing = kSOffLog + 4 * kSLogCap;
-constexpr uint32_t kSWarpBytes = kSOffRing + 480 + 16;  // ring, shaded colour cache
+constexpr uint32_t kSOffShd = kSOffRing + 480 + 16;     // after the ring and the shaded colour cache
+constexpr uint32_t kSWarpBytes = kSOffShd + 2 * kShdEntries;
 constexpr uint32_t kSWarps = CULE_SWARPS;  // warps per block (each warp emulates one env at a time)
 constexpr uint32_t kSmSDecode = kSmRom;  // scalar decode table [256] u64 right after the gray LUT
 constexpr uint32_t kSDecBytes = 2048;
@@ -66,6 +67,7 @@ __device__ __forceinline__ void load_smach(SMach* M, const Hdr& h, const Params&
   M->coll = hw(h, 5) & 0xFFFFu;
   M->pa_T = 0xFFFFFFFFu;
   M->idle_skip = p.idle_skip;
+  M->shd = 0u;  // no write elision unless the engine sets up a shadow (R#37)
   tw[0] = hw(h, 7);
   tw[1] = pk(hb(h, 35), hb(h, 36), hb(h, 37), hb(h, 32));
   tw[2] = pk(hb(h, 26), hb(h, 27), hb(h, 38), hb(h, 39));
@@ -267,6 +269,11 @@ __device__ __forceinline__ void scalar_env(const Params& p, uint32_t i, uint32_t
       set_inputs_s(M, p.actions[i]);
     }
   }
+#if defined(CULE_JIT) && !defined(CULE_VJIT)
+  // the translated engine drops TIA writes that change nothing (R#37): shadow unknown at step start
+  shd_init_warp(smem_addr(wb + kSOffShd), lane);
+  if (lane == 0u) M->shd = smem_addr(wb + kSOffShd);
+#endif
   __syncwarp();
   uint8_t* frame_out = kDebug ? nullptr
                               : (kGray ? p.staging + (size_t)i * (2 * kFrameBytes) : p.obs + (size_t)i * kFrameBytes);

@@ -23,6 +23,17 @@
 
 namespace cule {
 
+// TIA registers whose write is a pure store of the value (DESIGN.md §2 R#37): NUSIZ0 ... PF2
+// (0x04-0x0F) and ENAM0 ... RESMP1 (0x1D-0x29); scalar_cpu.cuh shd_write, jit.h
+constexpr uint64_t kTiaPure = (0xFFFull << 0x04) | (0x1FFFull << 0x1D);
+// shadow entry of TIA register r in 0x04-0x0F / 0x1B-0x29 (0..26); 27-29 the VDEL copies GRP0
+// old, GRP1 old, ENABL old; 32 u16 entries in all (scalar_cpu.cuh shd_write)
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+__host__ __device__
+#endif
+constexpr uint32_t shd_idx(uint32_t r) { return r <= 0x0Fu ? r - 0x04u : r - 0x1Bu + 12u; }
+constexpr uint32_t kShdG0o = 27u, kShdG1o = 28u, kShdEbo = 29u, kShdEntries = 32u;
+
 namespace pd {
 // Record word lo: [0:5) class, [5:8) aux, [8:12) base cycles (C_BR: cycles when taken),
 // [12:14) length, [20:32) low 12 bits of the fall-through PC (the instruction ends inside the

@@ -156,7 +156,7 @@ struct TiaP {
         const uint32_t line = T / 228u, h = T - line * 228u;
         if (h < 68u) w5 = (w5 & 0xFFFFu) | ((line & 0xFFFFu) << 16);
       } break;
-      case 0x2B: w3 &= 0x0000FFFFu; w4 = 0u; break;  // HMCLR
+      case 0x2B: w3 &= 0x0000FFFFu; w4 &= 0xFF000000u; break;  // HMCLR (byte 3: RESxx start delay, R#36)
       case 0x2C: w7 &= 0xFFFFu; break;               // CXCLR
       default: break;
     }

@@ -480,10 +480,15 @@ def _delay_programs():
     # a frame that ends (VSYNC) on the line of a visible RESP0: the start delay is pending at the
     # frame boundary (snapshot byte 63) and shows on the next frame's line 0 (window at ystart 0)
     out.append(micro.m23_resp_at_vsync())
+    # HMCLR right after a visible RESP0 on the same line: the start delay stays (R#36 is cleared
+    # only by the line end; HMCLR zeroes the motion registers alone), so the first copy stays dark
+    row0 = "    NOP\n" * 10 + "    STA $10\n    STA $2B\n"
+    out.append(micro.static_frame(pokes=[(0x09, 0x1E), (0x06, 0x86), (0x1B, 0xFF), (0x04, 0), (0x0D, 0xF0)],
+                                  positions=[(0x10, 10)], kernel_row0=row0, store_collisions=True))
     return out
 
 
-@pytest.mark.parametrize("case", range(7))
+@pytest.mark.parametrize("case", range(8))
 def test_tia_delays_static_frames_raw(case):
     """Static frames with mid-line playfield, GRP and RESxx writes, RAW frames every step, with
     the delayed register effects on (R#35, R#36): frames, collision latches and the state
