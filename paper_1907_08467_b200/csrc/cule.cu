@@ -493,15 +493,13 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     delete e;
     return fail(CULE_E_ROM_FAULT, "reset-cache build hit a JAM or runaway frame");
   }
-  // the translated engine: explicitly requested, or AUTO where it wins (measured sweep,
-  // profiles/r02_engine_sweep.txt: one ROM at every env count; mixed ROM sets up to 16384 envs —
-  // beyond that the batched engine amortises its datapath over 32 envs per warp and the
-  // translated code of several ROMs crowds the instruction cache) and applies (idle skip off)
-  // translated engines (measured sweep, profiles/r02_engine_sweep.txt): VJIT (one env per lane)
-  // from 8192 envs, or 4096 when several ROMs make the one-env-per-warp engine's replay the
-  // larger cost; else JIT (one env per warp); neither has the idle-loop skip
+  // the translated engines: explicitly requested, or AUTO where they apply (idle skip off)
+  // translated engines (measured crossover after the JIT engine's TIA write elision, R#37,
+  // profiles/r02_crossover_v77.txt): VJIT (one env per lane) from 16384 envs; below that JIT
+  // (one env per warp), for one ROM (8192 envs: 9.4M vs 7.5M FPS) and for the 4-ROM mix
+  // (5.25M vs 5.13M); neither has the idle-loop skip
   const bool xlate = !cfg->idle_skip;
-  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && (num_envs >= 8192 || (n_roms > 1 && num_envs >= 4096));
+  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && num_envs >= 16384;
   bool jit_auto = want == CULE_ENGINE_AUTO && xlate && !vjit_auto && (n_roms == 1 || num_envs <= 16384);
   if (want == CULE_ENGINE_VJIT || want == CULE_ENGINE_WSVJIT || vjit_auto) {
     const bool ws = want == CULE_ENGINE_WSVJIT;

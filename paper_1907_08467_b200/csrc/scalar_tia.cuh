@@ -283,11 +283,18 @@ __device__ __noinline__ void area84_row(uint32_t ring_s, uint32_t cols_s, uint32
   for (uint32_t j = lane; j < 84u; j += 32u) {
     uint32_t cw;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw) : "r"(cols_s + 4u * j) : "memory");
-    const uint32_t c0 = cw & 0xFFu, wc0 = (cw >> 8) & 0xFFu, wc1 = (cw >> 16) & 0xFFu, wc2 = cw >> 24;
-    const uint32_t c2 = wc2 ? c0 + 2u : c0;  // (weight 0: any in-row column)
-    const uint32_t s0 = wc0 * lds_u8(q0 + c0) + wc1 * lds_u8(q0 + c0 + 1u) + wc2 * lds_u8(q0 + c2);
-    const uint32_t s1 = wc0 * lds_u8(q1 + c0) + wc1 * lds_u8(q1 + c0 + 1u) + wc2 * lds_u8(q1 + c2);
-    const uint32_t s2 = wc0 * lds_u8(q2 + c0) + wc1 * lds_u8(q2 + c0 + 1u) + wc2 * lds_u8(q2 + c2);
+    // the three weighted input columns c0..c0+2 of each row: two aligned words, a funnel shift
+    // to bring byte c0 to the bottom, one dp4a with the packed weights wc0 | wc1 << 8 | wc2 << 16
+    // (byte 3 weight 0; a zero-weight byte past the row end reads the next ring row or the
+    // shaded-colour cache, both inside the warp's area)
+    const uint32_t c0 = cw & 0xFFu, wpk = cw >> 8, a4 = c0 & ~3u, sh = 8u * (c0 & 3u);
+    auto rowsum = [&](uint32_t q) {
+      uint32_t lo, hi;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(q + a4) : "memory");
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(hi) : "r"(q + a4 + 4u) : "memory");
+      return __dp4a(__funnelshift_r(lo, hi, sh), wpk, 0u);
+    };
+    const uint32_t s0 = rowsum(q0), s1 = rowsum(q1), s2 = rowsum(q2);
     const uint32_t S = w0 * s0 + 2u * s1 + w2 * s2;
     uint32_t q = S / 200u;
     const uint32_t r = S - 200u * q;
@@ -426,17 +433,23 @@ __device__ __forceinline__ void catch_up_coop(TiaP& t, uint32_t t_to, RowBuf& rb
   for (uint32_t ln = la; ln <= lb; ++ln) {
     const uint32_t xa = ln == l0 ? xa0 : 0u, xb = ln == l1 ? xb1 : 160u;
     if (xb <= xa) continue;
-    // pixels [xa, xb) of this lane's chunk [cx, cx+16) as a 16-bit mask (0 for lanes >= 10),
-    // merged branch-free: bit k of the mask <-> byte k % 4 of word k / 4
-    const uint32_t a = xa > cx ? min(xa - cx, 16u) : 0u, b = xb > cx ? min(xb - cx, 16u) : 0u;
-    const uint32_t pm = b > a ? (0xFFFFu >> (16u - (b - a))) << a : 0u;
-    const bool cb = (int32_t)ln == comb && lane == 0u;  // HMOVE comb: x < 8 black (R#11)
-    const uint32_t p0 = cb ? rb.fill : x0w, p1 = cb ? rb.fill : x1w;
-    const uint32_t m0 = nib_bytes(pm), m1 = nib_bytes(pm >> 4), m2 = nib_bytes(pm >> 8), m3 = nib_bytes(pm >> 12);
-    rb.r0 = (rb.r0 & ~m0) | (p0 & m0);
-    rb.r1 = (rb.r1 & ~m1) | (p1 & m1);
-    rb.r2 = (rb.r2 & ~m2) | (x2w & m2);
-    rb.r3 = (rb.r3 & ~m3) | (x3w & m3);
+    if (xa == 0u && xb == 160u && (int32_t)ln != comb) {
+      // the whole line in one span (the common case once writes that change nothing are
+      // dropped, R#37): every pixel of the chunk (lanes >= 10 hold the fill either way)
+      rb.r0 = x0w; rb.r1 = x1w; rb.r2 = x2w; rb.r3 = x3w;
+    } else {
+      // pixels [xa, xb) of this lane's chunk [cx, cx+16) as a 16-bit mask (0 for lanes >= 10),
+      // merged branch-free: bit k of the mask <-> byte k % 4 of word k / 4
+      const uint32_t a = xa > cx ? min(xa - cx, 16u) : 0u, b = xb > cx ? min(xb - cx, 16u) : 0u;
+      const uint32_t pm = b > a ? (0xFFFFu >> (16u - (b - a))) << a : 0u;
+      const bool cb = (int32_t)ln == comb && lane == 0u;  // HMOVE comb: x < 8 black (R#11)
+      const uint32_t p0 = cb ? rb.fill : x0w, p1 = cb ? rb.fill : x1w;
+      const uint32_t m0 = nib_bytes(pm), m1 = nib_bytes(pm >> 4), m2 = nib_bytes(pm >> 8), m3 = nib_bytes(pm >> 12);
+      rb.r0 = (rb.r0 & ~m0) | (p0 & m0);
+      rb.r1 = (rb.r1 & ~m1) | (p1 & m1);
+      rb.r2 = (rb.r2 & ~m2) | (x2w & m2);
+      rb.r3 = (rb.r3 & ~m3) | (x3w & m3);
+    }
     if (xb == 160u) row_done(rb, lane);
   }
 }
