@@ -125,10 +125,14 @@ RomSet make_romset(const uint8_t* const* roms, const size_t* rom_lens, int n_rom
 std::vector<char> jit_cubin(const RomSet& rs, int n_roms, bool gray, bool simt, bool ws, bool delays, size_t* n_insn,
                             double* secs, bool* from_disk, std::string& err, uint32_t vlogcap = 32) {
   cule::jit::Translator tr(rs.img.data(), rs.rom_off, rs.banks, n_roms, rs.bytes, rs.recs.data());
+  if (const char* v = getenv("CULE_VELIDE")) tr.vnoelide_ = !strcmp(v, "0");  // ablation switch
   cule::jit::Translation t = tr.run(gray, simt, ws);
   if (!t.ok) { err = t.why; return {}; }
   // ablation switch (measurement only): rebuild every coverage mask on every span
   if (getenv("CULE_TIA_NO_MASK_CACHE")) t.source = "#define CULE_TIA_NO_MASK_CACHE 1\n" + t.source;
+  // ablation switch (measurement only): VJIT block scheduler by __match_any_sync, largest group first
+  if (const char* v = getenv("CULE_VSCHED"))
+    if (simt && !strcmp(v, "match")) t.source = "#define CULE_VSCHED_MATCH 1\n" + t.source;
   // the kernel is compiled for one setting of the delayed register effects (tia.cuh CULE_DELAYS_ON)
   t.source = std::string("#define CULE_TIA_DELAYS ") + (delays ? "1" : "0") + "\n" + t.source;
   if (simt && !ws && vlogcap != 32) t.source = "#define CULE_VLOGCAP " + std::to_string(vlogcap) + "\n" + t.source;

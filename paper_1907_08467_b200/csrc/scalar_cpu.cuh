@@ -108,6 +108,9 @@ __device__ __forceinline__ bool shd_write(uint32_t shd, uint32_t r, uint32_t v) 
   return true;
 }
 
+// (out of line: the per-lane engine's translated code calls it from many sites)
+__device__ __noinline__ bool shd_write_ool(uint32_t shd, uint32_t r, uint32_t v) { return shd_write(shd, r, v); }
+
 __device__ __forceinline__ uint32_t s_coll_bits(uint32_t coll, uint32_t r) {
   return (((coll >> (2 * r)) & 1u) << 7) | (((coll >> (2 * r + 1)) & 1u) << 6);
 }
@@ -361,7 +364,15 @@ __device__ __noinline__ uint32_t s_gen_one(SMach* M, uint32_t rom_all0, uint32_t
           st_ram(ram0 + (a & 0x7Fu), val & 0xFFu);
         } else if (!(a & 0x1080u)) {  // TIA: effect registers go to the log (R#4)
           const uint32_t r = a & 0x3Fu;
+          // R#37: the shadow follows every logged write; the one-env-per-warp engine drops a
+          // write that changes nothing, the per-lane engines log it (their lanes' logs stay
+          // aligned; the translated code drops by warp vote, jit.h emit_simt)
+#ifdef CULE_VJIT
+          if ((kTiaEffect >> r) & 1ull) {
+            if (M->shd) (void)shd_write(M->shd, r, val & 0xFFu);
+#else
           if (((kTiaEffect >> r) & 1ull) && (!M->shd || shd_write(M->shd, r, val & 0xFFu))) {
+#endif
             st_log(lg0 + 4u * log_len, ((3u * now) << 14) | (r << 8) | (val & 0xFFu));
             ++log_len;
           } else if (r == 0x02u) {

@@ -11,8 +11,9 @@
 // lane is parked or idle, each lane replays its own TIA write log (tia.cuh flush_lane: the
 // batched engine's per-lane renderer), then the lanes resume.
 //
-// Shared memory per lane, 115 words (odd, so the same field of the 32 lanes falls in 32
-// different banks): TIA words 9 | pixel writer 9 | SMach 32 | RAM 32 | TIA log 32 + 1.
+// Shared memory per lane, 131 words (odd, so the same field of the 32 lanes falls in 32
+// different banks): TIA words 9 | pixel writer 9 | SMach 32 | RAM 32 | TIA log 32 + 1 | TIA write
+// shadow 16 (R#37; log capacity 64: 163 words).
 #pragma once
 
 namespace cule {
@@ -29,7 +30,9 @@ namespace cule {
 constexpr uint32_t kVLogCap = CULE_VLOGCAP;
 constexpr uint32_t kWLogCap = 32;  // per buffer, warp-specialized variant
 constexpr uint32_t kVOffTw = 0, kVOffPw = 9, kVOffM = 18, kVOffRam = 50, kVOffLog = 82;
-__host__ __device__ constexpr uint32_t vjit_lane_words(uint32_t cap) { return kVOffLog + cap + 1u; }
+// + the TIA write shadow (R#37: kShdEntries u16, 16 words) after the log
+__host__ __device__ constexpr uint32_t vjit_lane_words(uint32_t cap) { return kVOffLog + cap + 1u + kShdEntries / 2u; }
+constexpr uint32_t kVOffShd = kVOffLog + kVLogCap + 1u;
 constexpr uint32_t kVLaneWords = vjit_lane_words(kVLogCap);
 static_assert(kVLaneWords % 2 == 1 && vjit_lane_words(64u) % 2 == 1, "odd lane stride: conflict-free fields");
 static_assert(sizeof(SMach) == 4 * (kVOffRam - kVOffM), "SMach slot");
@@ -234,6 +237,8 @@ __device__ __forceinline__ void vjit_kernel_body(const Params& p) {
     for (int k = 0; k < 4; ++k) h.c[k] = st[k * N + i];
     rom_id = hb(h, 61);
     load_smach(M, h, p, tw);
+    M->shd = smem_addr(lw + kVOffShd);  // TIA write elision (R#37): every entry unknown at step start
+    shd_init_lane(M->shd);
     pw[8] = 0u;  // pixel writer idle until a rendered frame begins
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
