@@ -498,12 +498,13 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     return fail(CULE_E_ROM_FAULT, "reset-cache build hit a JAM or runaway frame");
   }
   // the translated engines: explicitly requested, or AUTO where they apply (idle skip off)
-  // translated engines (measured crossover after the JIT engine's TIA write elision, R#37,
-  // profiles/r02_crossover_v77.txt): VJIT (one env per lane) from 16384 envs; below that JIT
-  // (one env per warp), for one ROM (8192 envs: 9.4M vs 7.5M FPS) and for the 4-ROM mix
-  // (5.25M vs 5.13M); neither has the idle-loop skip
+  // translated engines (measured crossover with the TIA write elision in both, R#37,
+  // profiles/r02_crossover_v77.txt and profiles/r02_v78_pytest_gpu.txt): VJIT (one env per lane)
+  // from 16384 envs, or from 8192 with several ROMs (8192 envs of the 4-ROM mix: 6.83M vs 5.14M
+  // FPS); below that JIT (one env per warp; 8192 envs of one ROM: 9.39M vs 8.51M); neither has
+  // the idle-loop skip
   const bool xlate = !cfg->idle_skip;
-  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && num_envs >= 16384;
+  const bool vjit_auto = want == CULE_ENGINE_AUTO && xlate && (num_envs >= 16384 || (n_roms > 1 && num_envs >= 8192));
   bool jit_auto = want == CULE_ENGINE_AUTO && xlate && !vjit_auto && (n_roms == 1 || num_envs <= 16384);
   if (want == CULE_ENGINE_VJIT || want == CULE_ENGINE_WSVJIT || vjit_auto) {
     const bool ws = want == CULE_ENGINE_WSVJIT;
