@@ -242,16 +242,26 @@ class NatureCNN:
         self.w3, self.b3 = p(64, 64, 3, 3, fan=576), torch.zeros(64, device=dev, dtype=torch.bfloat16)
         self.w4, self.b4 = p(512, 3136, fan=3136), torch.zeros(512, device=dev, dtype=torch.bfloat16)
         self.w5, self.b5 = p(18, 512, fan=512), torch.zeros(18, device=dev, dtype=torch.bfloat16)
+        # conv1 per ring position of the newest frame: input channels permuted (the frames stay in
+        # place) and the 1/255 input scale folded into the weights; channels-last activations
+        # (cuDNN's NHWC kernels), algorithms picked by cudnn.benchmark at the warm-up steps
+        torch.backends.cudnn.benchmark = True
+        self.w1s = []
+        for slot in range(4):
+            order = [(slot + 1 + k) % 4 for k in range(4)]  # oldest -> newest ring slots
+            inv = [order.index(c) for c in range(4)]         # ring slot c holds temporal frame inv[c]
+            self.w1s.append((self.w1[:, inv].float() / 255.0).to(torch.bfloat16)
+                            .contiguous(memory_format=torch.channels_last))
+        self.w2 = self.w2.contiguous(memory_format=torch.channels_last)
+        self.w3 = self.w3.contiguous(memory_format=torch.channels_last)
 
     def act(self, stack, slot, gen):
         """Sample actions from the stack as the step kernel left it: slot `slot` is the newest
         frame, so conv1's input channels are permuted instead of the frames (no copy)."""
         import torch
         import torch.nn.functional as F
-        order = [(slot + 1 + k) % 4 for k in range(4)]      # oldest -> newest ring slots
-        inv = [order.index(c) for c in range(4)]             # ring slot c holds temporal frame inv[c]
-        x = stack.to(torch.bfloat16).mul_(1.0 / 255.0)
-        h = F.relu(F.conv2d(x, self.w1[:, inv], self.b1, stride=4))
+        x = stack.to(dtype=torch.bfloat16, memory_format=torch.channels_last)
+        h = F.relu(F.conv2d(x, self.w1s[slot], self.b1, stride=4))
         h = F.relu(F.conv2d(h, self.w2, self.b2, stride=2))
         h = F.relu(F.conv2d(h, self.w3, self.b3, stride=1))
         h = F.relu(F.linear(h.flatten(1), self.w4, self.b4))
