@@ -17,11 +17,11 @@ from paper_1907_08467_b200.inputs import micro
 BASE = [(0x09, 0x1E), (0x08, 0x44), (0x06, 0x86), (0x07, 0xC8), (0x1B, 0xF3), (0x1C, 0xC1), (0x04, 0x01),
         (0x05, 0x00), (0x0D, 0x50), (0x0E, 0xF0), (0x0F, 0x0F), (0x0A, 0x01), (0x1D, 0x02), (0x1E, 0x02),
         (0x1F, 0x02), (0x0B, 0x00), (0x0C, 0x08), (0x20, 0x10), (0x22, 0xF0), (0x25, 0x00), (0x27, 0x00),
-        (0x28, 0x00)]
+        (0x28, 0x00), (0x21, 0x20), (0x23, 0x00), (0x24, 0x10), (0x26, 0x00), (0x29, 0x00)]
 HELD = dict(BASE)
 VISIBLE = {0x09: 0x3A, 0x08: 0x9C, 0x06: 0x24, 0x07: 0x62, 0x04: 0x03, 0x05: 0x06, 0x0D: 0xA0, 0x0E: 0x0F,
            0x0F: 0xF0, 0x0A: 0x05, 0x1D: 0x00, 0x1E: 0x00, 0x1F: 0x00, 0x0B: 0x08, 0x0C: 0x00}
-OTHER_PURE = [0x20, 0x22, 0x25, 0x27, 0x28]  # HMP0, HMM0, VDELP0, VDELBL, RESMP0: no visible change expected
+OTHER_PURE = [0x20, 0x21, 0x22, 0x23, 0x24, 0x25, 0x26, 0x27, 0x28, 0x29]  # HMxx, VDELxx, RESMPx
 POS = [(0x10, 12), (0x11, 16), (0x12, 20), (0x13, 24), (0x14, 28)]
 
 
