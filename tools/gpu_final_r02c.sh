@@ -1,0 +1,8 @@
+#!/bin/bash
+# last check of HEAD: smoke, the default bench line (the driver's command), the AUTO-engine / frame-stack parity cases
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || true
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
+timeout 1200 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
+python -c "import json; d=json.loads(open('gpurun_out/bench_default.json').read().strip().splitlines()[-1]); print('bench', round(d['value']), d['ms_per_step'], d['config']['engine'], round(d['e2e']['value']), round(d['inference']['value']), d['clocks'])"
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_abi.py -q -m gpu -x -k "mixed_roms or num_envs or frame_stack or launch_shape or abi" > gpurun_out/pytest_c.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_c.log
