@@ -535,6 +535,18 @@ int cule_create(const uint8_t* const* roms, const size_t* rom_lens, int n_roms, 
     const uint32_t fit = (uint32_t)(((size_t)optin - lane_off) /
                                     (32u * 4u * (ws ? cule::kWLaneWords : cule::vjit_lane_words(vcap))));
     wpb = std::max(1u, std::min({wpb, fit, (uint32_t)CULE_VWARPS / (ws ? 2u : 1u)}));
+    // more warps than one wave of blocks holds (e.g. 65536 envs): equal waves of smaller blocks,
+    // so every SM runs whole waves instead of a short second one, with the log capacity they allow
+    if (!ws && !getenv("CULE_VWPB") && !getenv("CULE_VLOGCAP")) {
+      const uint32_t sm = (uint32_t)sm_count(), per_wave = wpb * sm;
+      if (warps > per_wave) {
+        const uint32_t waves = (warps + per_wave - 1) / per_wave;
+        const uint32_t w2 = (warps + waves * sm - 1) / (waves * sm);
+        const uint32_t cap2 = w2 <= 8u ? 64u : 32u;
+        const uint32_t fit2 = (uint32_t)(((size_t)optin - lane_off) / (32u * 4u * cule::vjit_lane_words(cap2)));
+        if (w2 >= 1u && w2 <= fit2) { wpb = w2; vcap = cap2; }
+      }
+    }
     e->vepw = vepw;
     e->vws = ws;
     e->vblock = (ws ? 64u : 32u) * wpb;
